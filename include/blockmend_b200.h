@@ -1,0 +1,174 @@
+/*
+ * blockmend_b200.h — C ABI of the B200-native concealment hot path.
+ *
+ * This is the drop-in boundary for the reference package `blockmend`
+ * (/root/reference/pkg/src/blockmend).  The reference is pure Python, so the
+ * "FFI a maintainer would bind" is ctypes; INTEGRATION.md shows the stub.
+ * Every entry point below names the reference interface it replaces.
+ *
+ * Conventions
+ *  - All pointers passed to bm_conceal / bm_estimate_batch are DEVICE pointers
+ *    (caller-owned, e.g. torch tensors' data_ptr()); the stream is a
+ *    cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - bm_conceal_host takes HOST pointers and does the host<->device copies
+ *    itself (pinned staging), i.e. the call a non-torch user makes.
+ *  - Status codes map onto the reference's exceptions (errors.py:4-25,
+ *    image.py:122-124, profiles.py:305); see bm_status_string().
+ *  - No CPU fallback: every compute entry point launches sm_100a kernels and
+ *    fails with BM_ERR_CUDA when no device is present.
+ */
+#ifndef BLOCKMEND_B200_H
+#define BLOCKMEND_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BM_ABI_VERSION 1
+
+/* status codes */
+#define BM_OK 0
+#define BM_ERR_ARGS 1       /* bad shape / argument  -> ValueError / DimensionMismatchError (image.py:122-124) */
+#define BM_ERR_LOST_LEFT 2  /* LOST pixels outside the 16x16 block grid remain -> AssertionError (profiles.py:305) */
+#define BM_ERR_CUDA 3       /* CUDA runtime error / no device */
+#define BM_ERR_WORKSPACE 4  /* workspace too small */
+#define BM_ERR_STATES 5     /* a state value > 2 -> ValueError (image.py:69-70) */
+
+/* layers (estimators.py:39-42); -1 = deferred mid-gray fill (profiles.py:215-225) */
+#define BM_LAYER_NONE (-1)
+#define BM_LAYER_BRL 0
+#define BM_LAYER_IDL 1
+#define BM_LAYER_HQL 2
+
+/* pixel dtypes of the input frames */
+#define BM_PIX_U8 0
+#define BM_PIX_F64 1
+
+/* bm_patch_record.flags */
+#define BM_REC_FALLBACK 1u  /* LayerDecision.fallback      (profiles.py:90) */
+#define BM_REC_DEFERRED 2u  /* LayerDecision.deferred_fill (profiles.py:91) */
+#define BM_REC_HAS_NU 4u    /* LayerDecision.nu is not None */
+#define BM_REC_HAS_PHI 8u   /* LayerDecision.phi is not None */
+#define BM_REC_HAS_BW 16u   /* LayerDecision.beta/alpha are not None (HQL) */
+#define BM_REC_HAS_M 32u    /* LayerDecision.m_candidates is not None */
+
+/* Run parameters: Profile (profiles.py:49-78) + conceal_image keywords
+ * (profiles.py:263-271). */
+typedef struct bm_params {
+  int32_t frames;       /* B: frames in the batch (conceal_image is B = 1) */
+  int32_t height;       /* H */
+  int32_t width;        /* W */
+  int32_t pixel_dtype;  /* BM_PIX_U8 or BM_PIX_F64 */
+  double t_phi;         /* Profile.t_phi */
+  double t_nu;          /* Profile.t_nu (may be +inf: sentinel) */
+  double sigma2;        /* DEFAULT_SIGMA2 = 10 (estimators.py:31) */
+  int32_t forced_layer; /* -1 = gated (select_and_estimate), else BM_LAYER_* (_forced_estimate) */
+  int32_t flags;        /* reserved, 0 */
+} bm_params;
+
+/* One LayerDecision (profiles.py:81-95) in the reference's order
+ * (lost cell raster order, then schedule/deferral order). 64 bytes. */
+typedef struct bm_patch_record {
+  int32_t frame;
+  int32_t row, col;     /* patch_origin */
+  int8_t layer;         /* BM_LAYER_* ; -1 for a deferred fill */
+  uint8_t flags;        /* BM_REC_* */
+  uint8_t n_y;          /* usable context count N_y (0 for deferred fills) */
+  uint8_t rings_used;   /* LayerDecision.rings_used */
+  int32_t m_candidates; /* valid if BM_REC_HAS_M */
+  uint32_t cycles;      /* SM clock cycles spent on the patch (-> elapsed_s) */
+  float beta_gap;       /* HQL: min over other grid betas of (eps_g - eps_best)/eps_best;
+                           a near-tie (< ~1e-12) is rounding-decided (parity harness) */
+  uint32_t pad;
+  double phi, nu, beta, alpha;
+} bm_patch_record;
+
+/* Per-batch summary (ConcealmentReport counts, metrics.py:21-43). */
+typedef struct bm_summary {
+  int64_t lost_cells;     /* lost 16x16 cells concealed (the throughput unit) */
+  int64_t patches;        /* records produced (incl. deferred fills) */
+  int64_t layer_counts[3];/* BRL, IDL, HQL (fallbacks counted under the layer used, profiles.py:309-314) */
+  int64_t deferred_fills;
+  int64_t lost_left;      /* LOST pixels outside the block grid (must be 0) */
+  int32_t max_level;      /* depth of the cross-cell dependency DAG */
+  int32_t pad;
+} bm_summary;
+
+/* ---- queries ---- */
+int bm_abi_version(void);
+const char* bm_status_string(int status);
+/* bytes of device workspace bm_conceal needs for these params */
+size_t bm_workspace_bytes(const bm_params* p);
+/* upper bound on records (64 per 16x16 cell of the grid) */
+int64_t bm_max_records(const bm_params* p);
+/* SM clock of the current device in kHz (converts bm_patch_record.cycles to
+ * seconds for ConcealmentReport.patch_times); 0 when no device. */
+int bm_device_clock_khz(void);
+
+/*
+ * bm_conceal — replaces blockmend.conceal_image (profiles.py:263-323) for a
+ * batch of B frames: _lost_block_ids + the raster-order _conceal_block loop
+ * (profiles.py:238-302), select_and_estimate / _forced_estimate per patch
+ * (profiles.py:105-171), and ImageBuffer.quantized (image.py:53-56).
+ *
+ *   pixels      [B,H,W] u8 or f64 (device)            ImageBuffer.pixels
+ *   states      [B,H,W] u8 {0,1,2} (device)           LossMask.states
+ *   out_f64     [B,H,W] f64 or NULL                   returned ImageBuffer.pixels
+ *   out_u8      [B,H,W] u8  or NULL                   ImageBuffer.quantized()
+ *   out_records [bm_max_records] or NULL              report.decisions (slot layout,
+ *                                                     compact with bm_compact_records)
+ *   out_summary device bm_summary* or NULL
+ *   workspace   device, >= bm_workspace_bytes(p)
+ * Inputs are never modified.  Asynchronous on `stream`; returns BM_OK once
+ * enqueued (argument errors are reported synchronously).
+ */
+int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states,
+               double* out_f64, uint8_t* out_u8, bm_patch_record* out_records,
+               bm_summary* out_summary, void* workspace, size_t workspace_bytes,
+               void* stream);
+
+/*
+ * bm_compact_records — gathers the slot-layout records written by bm_conceal
+ * into the reference's decision order (device -> device).  Returns the count
+ * in *out_count (host).  Synchronises `stream`.
+ */
+int bm_compact_records(const bm_params* p, const bm_patch_record* slot_records,
+                       void* workspace, bm_patch_record* out_records,
+                       int64_t* out_count, void* stream);
+
+/*
+ * bm_conceal_host — the same call with HOST buffers: copies pixels/states to
+ * the device, runs bm_conceal, copies the u8 (and optionally f64) result and
+ * the summary back.  Device buffers are cached across calls per (B,H,W).
+ * out_records (host) may be NULL; when given it receives *out_nrec compacted
+ * records (capacity bm_max_records).
+ */
+int bm_conceal_host(const bm_params* p, const void* pixels, const uint8_t* states,
+                    double* out_f64, uint8_t* out_u8, bm_patch_record* out_records,
+                    int64_t* out_nrec, bm_summary* out_summary);
+
+/*
+ * bm_estimate_batch — per-instance estimator entry (device pointers):
+ * brl_estimate / idl_estimate / hql_estimate (estimators.py:96-132, 248-286)
+ * on `count` independent (target, candidate set) instances in dense layout.
+ *   layer       BM_LAYER_BRL / IDL / HQL (HQL includes its IDL->BRL ladder)
+ *   n_y[i]      context length of instance i (1..32)
+ *   m[i]        candidate count of instance i (0..max_m)
+ *   y0          [count][32]        target context (first n_y used)
+ *   x           [count][max_m][4]  candidate patch values
+ *   y           [count][max_m][32] candidate contexts (first n_y used)
+ *   out_values  [count][4]
+ *   out_info    [count] records: layer, flags (fallback), m, nu (IDL raw_sum), beta, alpha
+ */
+int bm_estimate_batch(int32_t layer, int32_t count, int32_t max_m, double sigma2,
+                      const int32_t* n_y, const int32_t* m, const double* y0,
+                      const double* x, const double* y, double* out_values,
+                      bm_patch_record* out_info, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BLOCKMEND_B200_H */

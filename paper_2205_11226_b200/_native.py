@@ -1,0 +1,138 @@
+"""Loader and ctypes bindings of the sm_100a extension (_blockmend_b200.so).
+
+The product path has no CPU fallback: if the shared library is missing or no
+CUDA device is present, every compute call raises NativeUnavailableError.
+`build()` compiles csrc/ in-tree with nvcc for sm_100a.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+from .errors import DimensionMismatchError, NativeUnavailableError
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
+SOURCES = [os.path.join(PKG_DIR, "csrc", "bm_conceal.cu")]
+HEADERS = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_common.cuh", "bm_estimators.cuh")] + [
+    os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
+]
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+BM_OK, BM_ERR_ARGS, BM_ERR_LOST_LEFT, BM_ERR_CUDA, BM_ERR_WORKSPACE, BM_ERR_STATES = 0, 1, 2, 3, 4, 5
+
+
+class Params(ctypes.Structure):
+    _fields_ = [
+        ("frames", ctypes.c_int32),
+        ("height", ctypes.c_int32),
+        ("width", ctypes.c_int32),
+        ("pixel_dtype", ctypes.c_int32),
+        ("t_phi", ctypes.c_double),
+        ("t_nu", ctypes.c_double),
+        ("sigma2", ctypes.c_double),
+        ("forced_layer", ctypes.c_int32),
+        ("flags", ctypes.c_int32),
+    ]
+
+
+class Summary(ctypes.Structure):
+    _fields_ = [
+        ("lost_cells", ctypes.c_int64),
+        ("patches", ctypes.c_int64),
+        ("layer_counts", ctypes.c_int64 * 3),
+        ("deferred_fills", ctypes.c_int64),
+        ("lost_left", ctypes.c_int64),
+        ("max_level", ctypes.c_int32),
+        ("pad", ctypes.c_int32),
+    ]
+
+
+SUMMARY_BYTES = ctypes.sizeof(Summary)
+EXPORTS = [
+    "bm_abi_version", "bm_status_string", "bm_workspace_bytes", "bm_max_records", "bm_device_clock_khz",
+    "bm_conceal", "bm_compact_records", "bm_conceal_host", "bm_estimate_batch",
+]
+
+
+def needs_build() -> bool:
+    if not os.path.exists(LIB_PATH):
+        return True
+    t = os.path.getmtime(LIB_PATH)
+    return any(os.path.getmtime(s) > t for s in SOURCES + HEADERS)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a ... -> _blockmend_b200.so (in-tree)."""
+    if not force and not needs_build():
+        return LIB_PATH
+    tmp = LIB_PATH + ".tmp"
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", tmp, *SOURCES]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    """The loaded extension; raises NativeUnavailableError if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeUnavailableError(
+            f"{LIB_PATH} is missing: build it with paper_2205_11226_b200._native.build() "
+            "(there is no CPU fallback)"
+        )
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+    L.bm_abi_version.restype = ctypes.c_int
+    L.bm_status_string.restype = ctypes.c_char_p
+    L.bm_status_string.argtypes = [ctypes.c_int]
+    L.bm_workspace_bytes.restype = ctypes.c_size_t
+    L.bm_workspace_bytes.argtypes = [ctypes.POINTER(Params)]
+    L.bm_max_records.restype = i64
+    L.bm_max_records.argtypes = [ctypes.POINTER(Params)]
+    L.bm_device_clock_khz.restype = ctypes.c_int
+    L.bm_conceal.restype = ctypes.c_int
+    L.bm_conceal.argtypes = [ctypes.POINTER(Params), vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
+    L.bm_compact_records.restype = ctypes.c_int
+    L.bm_compact_records.argtypes = [ctypes.POINTER(Params), vp, vp, vp, ctypes.POINTER(i64), vp]
+    L.bm_conceal_host.restype = ctypes.c_int
+    L.bm_conceal_host.argtypes = [ctypes.POINTER(Params), vp, vp, vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(Summary)]
+    L.bm_estimate_batch.restype = ctypes.c_int
+    L.bm_estimate_batch.argtypes = [i32, i32, i32, ctypes.c_double, vp, vp, vp, vp, vp, vp, vp, vp]
+    _lib = L
+    return L
+
+
+def check(status: int) -> None:
+    """Map a C-ABI status onto the reference's exceptions."""
+    if status == BM_OK:
+        return
+    msg = lib().bm_status_string(status).decode()
+    if status == BM_ERR_LOST_LEFT:
+        raise AssertionError(msg)  # profiles.py:305
+    if status == BM_ERR_STATES:
+        raise ValueError(msg)  # image.py:69-70
+    if status == BM_ERR_ARGS:
+        raise DimensionMismatchError(msg)
+    raise NativeUnavailableError(msg)
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise NativeUnavailableError("no CUDA device: the B200 path has no CPU fallback")
+    return torch

@@ -1,0 +1,1206 @@
+// bm_conceal.cu — the B200 concealment path: mask preprocessing (lost-cell
+// slots, dependency levels, ticket order), the persistent CTA-per-lost-cell
+// concealment kernel, the dense estimator kernel, and the C ABI
+// (include/blockmend_b200.h).
+//
+// Reference path: blockmend.conceal_image (profiles.py:263-323) ->
+// _conceal_block (profiles.py:191-226) -> select_and_estimate /
+// _forced_estimate (profiles.py:105-171) -> framework.py gather ->
+// estimators.py.
+//
+// Execution model:
+//  * one CTA conceals one lost 16x16 cell: it stages the cell's 48x48 support
+//    area (FP64 values, FP32 shadow, states, LOST bitmaps) in shared memory and
+//    runs the cell's whole <=64-patch reliability-ordered chain in place;
+//  * cells are handed out by an atomic ticket in (dependency level, frame,
+//    raster) order; a cell first waits (acquire) for its earlier-raster
+//    8-neighbour lost cells, which reproduces the reference's serial raster
+//    order exactly while independent cells run concurrently;
+//  * a finished cell publishes its 16x16 FP64 values to a per-cell buffer and
+//    releases its flag; later cells read neighbours from those buffers, so the
+//    working image never exists in HBM as a full FP64 copy.
+#include <cub/cub.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/blockmend_b200.h"
+#include "bm_common.cuh"
+#include "bm_estimators.cuh"
+
+namespace bm {
+
+struct KParams {
+  int B, H, W, GR, GC;
+  int pix_f64;
+  double t_phi, t_nu, sigma2;
+  int forced;
+  const void* pixels;
+  const uint8_t* states;
+  double* out_f64;
+  uint8_t* out_u8;
+  bm_patch_record* records;
+  // workspace
+  int* slotmap;        // [B*GR*GC] slot index or -1
+  int* slot_cell;      // [ncell] linear cell index of slot
+  unsigned* level;     // [ncell]
+  unsigned* order;     // [ncell] slots in ticket order
+  unsigned* done;      // [ncell]
+  int* nslots;         // [1]
+  unsigned* ticket;    // [1]
+  double* cellbuf;     // [ncell][256]
+  uint8_t* rec_count;  // [ncell]
+  unsigned long long* counters;  // [8]: BRL, IDL, HQL, deferred, lost_left, bad_states, patches, maxlevel
+  double* scratch;     // per-CTA HQL scratch
+  size_t scratch_per_cta;  // doubles
+};
+
+struct CellSmem {
+  double tile[TILE * TS];
+  float tile32[TILE * TS];
+  uint64_t lostbits[TILE];
+  uint8_t st[TILE * TS];
+  uint16_t cand[MAXCAND];
+  float d2f[MAXCAND];
+  float rbuf[NT];
+  int pref[NT];
+  int wcnt[NWARP];
+  int ring_off[MAXRING + 2];
+  // per-patch control (written by warp 0 / thread 0, read after a barrier)
+  int ticket, slot, f, gr, gc;
+  unsigned long long remaining, pend;
+  int deferred[64];
+  int ndef, progressed, nrec;
+  int pick, skip, gated_stop;
+  int m, m_total, rings_used, max_ring, K, cur_ring;
+  double nu, carry, phi;
+  unsigned rowmask[6];
+  long long t_start;
+  unsigned long long cnt[4];
+  EstSmem est;
+};
+
+__device__ __forceinline__ int patch_r(int p) { return BS + 2 * (p >> 3); }  // tile coords of patch p
+__device__ __forceinline__ int patch_c(int p) { return BS + 2 * (p & 7); }
+
+// ------------------------------------------------------------ preprocessing
+
+// lost flag per grid cell; LOST pixels outside the grid; state range check
+__global__ void k_cell_flags(KParams P, int* flags) {
+  const int GR = P.GR, GC = P.GC, H = P.H, W = P.W;
+  const size_t ncell = (size_t)P.B * GR * GC;
+  const int lane = threadIdx.x & 31;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t c = warp; c < ncell; c += nwarps) {
+    const int f = (int)(c / ((size_t)GR * GC));
+    const int rem = (int)(c % ((size_t)GR * GC));
+    const int gr = rem / GC, gc = rem % GC;
+    const uint8_t* s = P.states + ((size_t)f * H + gr * BS) * W + gc * BS;
+    // 256 states: lane reads 8 bytes (row lane/2, half lane&1)
+    const int r = lane >> 1, h = (lane & 1) * 8;
+    int lost = 0, bad = 0;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      uint8_t v = s[(size_t)r * W + h + i];
+      lost |= v == ST_LO;
+      bad |= v > ST_RE;
+    }
+    lost = __any_sync(FULL, lost);
+    bad = __any_sync(FULL, bad);
+    if (lane == 0) {
+      flags[c] = lost;
+      if (bad) atomicAdd(&P.counters[5], 1ull);
+    }
+  }
+  // ragged margins (pixels outside the full-cell grid)
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nthr = (size_t)gridDim.x * blockDim.x;
+  const int mr = H - GR * BS, mc = W - GC * BS;
+  const size_t per_frame = (size_t)mr * W + (size_t)(H - mr) * mc;
+  for (size_t i = tid; i < per_frame * P.B; i += nthr) {
+    const int f = (int)(i / per_frame);
+    size_t k = i % per_frame;
+    int r, c;
+    if (k < (size_t)mr * W) {
+      r = GR * BS + (int)(k / W);
+      c = (int)(k % W);
+    } else {
+      k -= (size_t)mr * W;
+      r = (int)(k / mc);
+      c = GC * BS + (int)(k % mc);
+    }
+    const uint8_t v = P.states[((size_t)f * H + r) * W + c];
+    if (v == ST_LO) atomicAdd(&P.counters[4], 1ull);
+    if (v > ST_RE) atomicAdd(&P.counters[5], 1ull);
+  }
+}
+
+__global__ void k_slots(KParams P, const int* flags, const int* excl) {
+  const size_t ncell = (size_t)P.B * P.GR * P.GC;
+  for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < ncell; c += (size_t)gridDim.x * blockDim.x) {
+    if (flags[c]) {
+      P.slotmap[c] = excl[c];
+      P.slot_cell[excl[c]] = (int)c;
+      P.done[excl[c]] = 0;
+    } else {
+      P.slotmap[c] = -1;
+    }
+    if (c == ncell - 1) *P.nslots = excl[c] + flags[c];
+  }
+}
+
+// Longest-path level of every lost cell in its frame's dependency DAG:
+// level(u) = 1 + max level of its lost earlier-raster 8-neighbours
+// ((r-1,c-1),(r-1,c),(r-1,c+1),(r,c-1)); one warp per frame, rows in order,
+// the left-neighbour chain inside a row as a max-plus warp scan.
+__global__ void k_levels(KParams P) {
+  const int lane = threadIdx.x & 31;
+  const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (f >= P.B) return;
+  const int GR = P.GR, GC = P.GC;
+  const int* sm = P.slotmap + (size_t)f * GR * GC;
+  unsigned maxlvl = 0;
+  for (int r = 0; r < GR; r++) {
+    int carry = -1000000;  // level(c-1) - (c-1) style carry across chunks: stores level of the cell left of chunk
+    int left_lost = 0;
+    for (int c0 = 0; c0 < GC; c0 += 32) {
+      const int c = c0 + lane;
+      int slot = c < GC ? sm[r * GC + c] : -1;
+      int base = -1;  // -1: not lost
+      if (slot >= 0) {
+        int b = 0;
+        if (r > 0) {
+          for (int dc = -1; dc <= 1; dc++) {
+            const int cc = c + dc;
+            if (cc < 0 || cc >= GC) continue;
+            const int s2 = sm[(r - 1) * GC + cc];
+            if (s2 >= 0) b = max(b, (int)P.level[s2] + 1);
+          }
+        }
+        base = b;
+      }
+      // chain: level(c) = max(base(c), level(c-1)+1) when c-1 is lost.
+      // value(c) = level(c) - c; run-segmented prefix max of (base - c).
+      const bool lost = slot >= 0;
+      int val = lost ? base - c : -1000000;
+      // segment starts where the left neighbour is not lost
+      const int up_lost = __shfl_up_sync(FULL, (int)lost, 1);
+      const bool prev_lost_inchunk = lane > 0 ? up_lost : left_lost;
+      int seg_start = lost && !prev_lost_inchunk;
+      // incorporate carry from previous chunk for lane 0 when left neighbour lost
+      if (lane == 0 && lost && left_lost) val = max(val, carry);
+      // inclusive segmented max-scan
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ov = __shfl_up_sync(FULL, val, o);
+        const int os = __shfl_up_sync(FULL, seg_start, o);
+        if (lane >= o && !seg_start) {
+          val = max(val, ov);
+          seg_start = os;
+        }
+      }
+      if (lost) {
+        const unsigned lv = (unsigned)(val + c);
+        P.level[slot] = lv;
+        maxlvl = max(maxlvl, lv);
+      }
+      carry = __shfl_sync(FULL, val, 31);
+      left_lost = __shfl_sync(FULL, (int)lost, 31);
+      __syncwarp();
+    }
+    __syncwarp();
+    __threadfence_block();
+  }
+  maxlvl = (unsigned)__reduce_max_sync(FULL, maxlvl);
+  if (lane == 0) atomicMax((unsigned long long*)&P.counters[7], (unsigned long long)maxlvl);
+}
+
+__global__ void k_iota(unsigned* v, const int* nslots, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = (unsigned)i;
+}
+
+// --------------------------------------------------------- the cell kernel
+
+__device__ void load_tile(const KParams& P, CellSmem& S) {
+  const int f = S.f, gr = S.gr, gc = S.gc;
+  const int R0 = gr * BS - BS, C0 = gc * BS - BS;
+  const int H = P.H, W = P.W;
+  for (int i = threadIdx.x; i < TILE * TILE; i += NT) {
+    const int tr = i / TILE, tc = i % TILE;
+    const int r = R0 + tr, c = C0 + tc;
+    double v = 0.0;
+    uint8_t s = ST_LO;  // out of image: never usable (framework.py:160)
+    if (r >= 0 && r < H && c >= 0 && c < W) {
+      const size_t o = ((size_t)f * H + r) * W + c;
+      s = P.states[o];
+      const int ntr = tr / BS, ntc = tc / BS;
+      const int nr = gr - 1 + ntr, nc = gc - 1 + ntc;
+      int pslot = -1;
+      if ((ntr == 0 || (ntr == 1 && ntc == 0)) && nr >= 0 && nc >= 0 && nc < P.GC)
+        pslot = P.slotmap[((size_t)f * P.GR + nr) * P.GC + nc];
+      if (pslot >= 0) {  // finished earlier-raster neighbour: its final values
+        v = __ldcg(&P.cellbuf[(size_t)pslot * 256 + (tr % BS) * BS + (tc % BS)]);
+        if (s == ST_LO) s = ST_RE;
+      } else {
+        v = P.pix_f64 ? ((const double*)P.pixels)[o] : (double)((const uint8_t*)P.pixels)[o];
+      }
+    }
+    S.tile[tr * TS + tc] = v;
+    S.tile32[tr * TS + tc] = (float)v;
+    S.st[tr * TS + tc] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < TILE) {
+    uint64_t b = 0;
+    for (int c = 0; c < TILE; c++) b |= (uint64_t)(S.st[threadIdx.x * TS + c] == ST_LO) << c;
+    S.lostbits[threadIdx.x] = b;
+  }
+  __syncthreads();
+}
+
+// Gather of the admissible candidates in (ring, row, col) order with the ring
+// by ring nu gate (profiles.py:113-124, framework.py:171-207), or the one-shot
+// full gather of _forced_estimate (profiles.py:148-149).  Sets S.m, rings_used,
+// nu; S.cand / S.d2f hold the candidates.
+__device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool gated) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  EstSmem& E = S.est;
+  const int n = E.n;
+  // geometry (absolute coordinates)
+  const int br = S.gr * BS, bc = S.gc * BS;
+  const int R0 = br - BS, C0 = bc - BS;
+  RingGeom g;
+  g.pr = R0 + pr_t;
+  g.pc = C0 + pc_t;
+  const int r0 = max(0, br - BS), r1 = min(P.H, br + 2 * BS);
+  const int c0 = max(0, bc - BS), c1 = min(P.W, bc + 2 * BS);
+  g.A0 = r0 + 2;
+  g.A1 = r1 - 4;
+  g.B0 = c0 + 2;
+  g.B1 = c1 - 4;
+  if (warp == 0) {
+    int cnt = (lane >= 1 && lane <= 26) ? ring_count(g, lane) : 0;
+    // inclusive scan
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(FULL, inc, o);
+      if (lane >= o) inc += v;
+    }
+    // ring_off[r] = sum of counts of rings < r
+    if (lane <= 27) S.ring_off[lane] = inc - cnt;  // lane 0 -> 0
+    unsigned nz = __ballot_sync(FULL, cnt > 0);
+    if (lane == 0) {
+      S.max_ring = nz ? 31 - __clz(nz) : 0;
+      S.K = S.ring_off[0] + 0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      S.K = S.max_ring ? S.ring_off[S.max_ring] + ring_count(g, S.max_ring) : 0;
+      S.ring_off[S.max_ring + 1] = S.K;
+      S.m = 0;
+      S.m_total = 0;
+      S.nu = 0.0;
+      S.carry = 0.0;
+      S.cur_ring = 0;  // rings fully accounted
+      S.gated_stop = 0;
+      S.rings_used = 0;
+    }
+  }
+  __syncthreads();
+  const int K = S.K, max_ring = S.max_ring;
+  if (max_ring == 0) {  // empty expansion map: exhausted before the first ring
+    if (tid == 0) { S.m = 0; S.rings_used = 0; }
+    __syncthreads();
+    return;
+  }
+  const float invf = (float)(1.0 / (2.0 * P.sigma2 * n));
+  for (int e0 = 0; e0 < K; e0 += NT) {
+    const int e = e0 + tid;
+    bool adm = false;
+    float d2 = 0.f, rw = 0.f;
+    int pos = 0;
+    if (e < K) {
+      int r = 1;
+      while (r < max_ring && S.ring_off[r + 1] <= e) r++;
+      int a, b;
+      ring_entry(g, r, e - S.ring_off[r], a, b);
+      const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
+      adm = true;
+#pragma unroll
+      for (int q = 0; q < 6; q++)
+        if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) adm = false;
+      if (adm) {
+        pos = wr * TS + wc;
+        const float* tp = S.tile32 + pos;
+        for (int k = 0; k < n; k++) {
+          const float d = tp[E.uoff[k]] - E.y0f[k];
+          d2 = fmaf(d, d, d2);
+        }
+        if (gated) rw = expf(-d2 * invf);  // raw_idl_weights (estimators.py:105-109)
+      }
+    }
+    // ordered compaction
+    const unsigned bal = __ballot_sync(FULL, adm);
+    const int wpre = __popc(bal & ((1u << lane) - 1));
+    if (lane == 0) S.wcnt[warp] = __popc(bal);
+    S.rbuf[tid] = adm ? rw : 0.f;
+    __syncthreads();
+    int base = 0, tot = 0;
+#pragma unroll
+    for (int w = 0; w < NWARP; w++) {
+      if (w < warp) base += S.wcnt[w];
+      tot += S.wcnt[w];
+    }
+    const int m0 = S.m_total;
+    if (adm) {
+      S.cand[m0 + base + wpre] = (uint16_t)pos;
+      S.d2f[m0 + base + wpre] = d2;
+    }
+    S.pref[tid] = base + wpre + (adm ? 1 : 0);  // inclusive count up to e
+    __syncthreads();
+    if (!gated) {
+      if (tid == 0) S.m_total = m0 + tot;
+      __syncthreads();
+      continue;
+    }
+    // nu bookkeeping, ring by ring (warp 0)
+    if (warp == 0) {
+      const int e1 = min(e0 + NT, K);
+      int r = S.cur_ring + 1;
+      double carry = S.carry, nu = S.nu;
+      int stop = 0;
+      while (r <= max_ring) {
+        const int lo = max(S.ring_off[r], e0), hi = min(S.ring_off[r + 1], e1);
+        double part = 0.0;
+        for (int i = lo + lane; i < hi; i += 32) part += (double)S.rbuf[i - e0];
+        part = warp_sum(part);
+        if (S.ring_off[r + 1] > e1) {  // ring continues in the next chunk
+          carry += part;
+          break;
+        }
+        nu += carry + part;  // nu += sum of the ring's raw weights
+        carry = 0.0;
+        if (!(nu < P.t_nu) || r >= max_ring) {
+          stop = 1;
+          if (lane == 0) {
+            S.rings_used = r;
+            const int end = S.ring_off[r + 1];
+            S.m = m0 + (end > e0 ? S.pref[end - e0 - 1] : 0);
+          }
+          break;
+        }
+        r++;
+      }
+      if (lane == 0) {
+        S.cur_ring = stop ? r : r - 1;
+        S.carry = carry;
+        S.nu = nu;
+        S.gated_stop = stop;
+        S.m_total = m0 + tot;
+      }
+    }
+    __syncthreads();
+    if (S.gated_stop) break;
+  }
+  if (!gated && tid == 0) {
+    S.m = S.m_total;
+    S.rings_used = max_ring;
+  }
+  __syncthreads();
+}
+
+__device__ void write_record(const KParams& P, CellSmem& S, const bm_patch_record& rec) {
+  if (P.records) P.records[(size_t)S.slot * 64 + S.nrec] = rec;
+}
+
+// One patch: gate + estimate (select_and_estimate / _forced_estimate).
+__device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV, double* gQ) {
+  const int tid = threadIdx.x;
+  EstSmem& E = S.est;
+  const int pr_t = patch_r(p), pc_t = patch_c(p);
+  const int forced = P.forced;
+  const bool brl = forced >= 0 ? forced == BM_LAYER_BRL : S.phi <= P.t_phi;
+  __shared__ bm_patch_record rec;
+  if (tid == 0) {
+    memset(&rec, 0, sizeof(rec));
+    rec.frame = S.f;
+    rec.row = S.gr * BS - BS + pr_t;
+    rec.col = S.gc * BS - BS + pc_t;
+    rec.phi = S.phi;
+    rec.nu = rec.beta = rec.alpha = __longlong_as_double(0x7ff8000000000000ll);
+    rec.flags = BM_REC_HAS_PHI | BM_REC_HAS_M;
+    rec.n_y = (uint8_t)E.n;
+    rec.beta_gap = __int_as_float(0x7fc00000);
+  }
+  if (brl) {
+    brl_values(E);
+    if (tid == 0) {
+      rec.layer = BM_LAYER_BRL;
+      rec.m_candidates = 0;
+      rec.rings_used = 0;
+    }
+    __syncthreads();
+  } else {
+    const bool gated = forced < 0;
+    gather(P, S, pr_t, pc_t, gated);
+    const int m = S.m;
+    TileAcc acc{S.tile, S.cand, E.uoff};
+    if (tid == 0) {
+      rec.rings_used = (uint8_t)S.rings_used;
+      rec.m_candidates = m;
+    }
+    if (gated && !(S.nu < P.t_nu)) {
+      // nu >= T_nu -> IDL (profiles.py:123-124); nu > 0 so no underflow
+      idl_estimate_dev(acc, S.d2f, m, P.sigma2, E);
+      if (tid == 0) {
+        rec.layer = BM_LAYER_IDL;
+        rec.nu = S.nu;
+        rec.flags |= BM_REC_HAS_NU;
+      }
+    } else if (forced == BM_LAYER_IDL) {  // profiles.py:144-153
+      bool ok = false;
+      if (m >= 1) {
+        idl_estimate_dev(acc, S.d2f, m, P.sigma2, E);
+        ok = E.ok;
+      }
+      if (ok) {
+        if (tid == 0) {
+          rec.layer = BM_LAYER_IDL;
+          rec.nu = E.nu_raw;
+          rec.flags |= BM_REC_HAS_NU;
+        }
+      } else {
+        brl_values(E);
+        if (tid == 0) {
+          rec.layer = BM_LAYER_BRL;
+          rec.m_candidates = 0;
+          rec.flags |= BM_REC_FALLBACK;
+        }
+      }
+    } else {
+      // HQL with its ladder (estimators.py:248-286)
+      bool done = false;
+      if (m >= 2) {
+        hql_core(acc, m, E, gV, gQ);
+        if (E.ok) {
+          done = true;
+          if (tid == 0) {
+            rec.layer = BM_LAYER_HQL;
+            rec.beta = E.beta;
+            rec.alpha = E.alpha;
+            rec.beta_gap = E.gap;
+            rec.flags |= BM_REC_HAS_BW;
+          }
+        }
+      }
+      if (!done && m >= 1) {
+        idl_estimate_dev(acc, S.d2f, m, P.sigma2, E);
+        if (E.ok) {
+          done = true;
+          if (tid == 0) {
+            rec.layer = BM_LAYER_IDL;
+            rec.flags |= BM_REC_FALLBACK;
+            if (!gated) {
+              rec.nu = E.nu_raw;
+              rec.flags |= BM_REC_HAS_NU;
+            }
+          }
+        }
+      }
+      if (!done) {
+        brl_values(E);
+        if (tid == 0) {
+          rec.layer = BM_LAYER_BRL;
+          rec.flags |= BM_REC_FALLBACK;
+        }
+      }
+      if (gated && tid == 0) {
+        rec.nu = S.nu;
+        rec.flags |= BM_REC_HAS_NU;
+      }
+    }
+    __syncthreads();
+  }
+  // write back (profiles.py:229-235) + record
+  if (tid < 4) {
+    const int o = (pr_t + (tid >> 1)) * TS + pc_t + (tid & 1);
+    if (S.st[o] == ST_LO) {
+      S.tile[o] = E.vals[tid];
+      S.tile32[o] = (float)E.vals[tid];
+      S.st[o] = ST_RE;
+    }
+  }
+  __syncthreads();
+  if (tid < 2) {
+    const int r = pr_t + tid;
+    uint64_t b = S.lostbits[r];
+    b &= ~(3ull << pc_t);
+    b |= (uint64_t)(S.st[r * TS + pc_t] == ST_LO) << pc_t;
+    b |= (uint64_t)(S.st[r * TS + pc_t + 1] == ST_LO) << (pc_t + 1);
+    S.lostbits[r] = b;
+  }
+  if (tid == 0) {
+    rec.cycles = (uint32_t)(clock64() - S.t_start);
+    write_record(P, S, rec);
+    S.nrec++;
+    S.cnt[rec.layer]++;
+  }
+  __syncthreads();
+}
+
+// pick_next_patch (framework.py:243-250) + extract_target (framework.py:151-168)
+// by warp 0.  Returns via S.pick / S.skip.
+__device__ void pick_and_extract(CellSmem& S) {
+  const int lane = threadIdx.x & 31;
+  EstSmem& E = S.est;
+  const unsigned long long pend = S.pend;
+  int best_key = -1;
+#pragma unroll
+  for (int h = 0; h < 2; h++) {
+    const int p = lane + 32 * h;
+    if ((pend >> p) & 1ull) {
+      const int pr = patch_r(p), pc = patch_c(p);
+      int av = 0, us = 0;
+#pragma unroll
+      for (int k = 0; k < 32; k++) {
+        const uint8_t s = S.st[(pr - 2 + ctx_r(k)) * TS + pc - 2 + ctx_c(k)];
+        av += s == ST_AV;
+        us += s != ST_LO;
+      }
+      const int key = (av << 13) | (us << 7) | (63 - p);
+      best_key = max(best_key, key);
+    }
+  }
+  best_key = __reduce_max_sync(FULL, (unsigned)(best_key + 1)) - 1;
+  const int p = 63 - (best_key & 127);
+  // extract target
+  const int pr = patch_r(p), pc = patch_c(p);
+  const int o = (pr - 2 + ctx_r(lane)) * TS + pc - 2 + ctx_c(lane);
+  const bool usable = S.st[o] != ST_LO;
+  const unsigned bal = __ballot_sync(FULL, usable);
+  const int n = __popc(bal);
+  if (usable) {
+    const int idx = __popc(bal & ((1u << lane) - 1));
+    E.y0[idx] = S.tile[o];
+    E.y0f[idx] = S.tile32[o];
+    E.uoff[idx] = (int16_t)(ctx_r(lane) * TS + ctx_c(lane));
+  }
+  // row masks of used window positions (usable context + patch cells)
+  unsigned rm = 0;
+  if (lane < 6) {
+    for (int k = 0; k < 32; k++)
+      if (((bal >> k) & 1u) && ctx_r(k) == lane) rm |= 1u << ctx_c(k);
+    if (lane == 2 || lane == 3) rm |= (1u << 2) | (1u << 3);
+    S.rowmask[lane] = rm;
+  }
+  __syncwarp();
+  if (lane < 4) E.uoff[n + lane] = (int16_t)((2 + (lane >> 1)) * TS + 2 + (lane & 1));
+  // flatness (profiles.py:98-102)
+  double ymax = usable ? S.tile[o] : -INFINITY, ymin = usable ? S.tile[o] : INFINITY;
+  ymax = warp_max(ymax);
+  ymin = warp_min(ymin);
+  if (lane == 0) {
+    S.pick = p;
+    S.pend = pend & ~(1ull << p);
+    E.n = n;
+    S.skip = n == 0;
+    S.phi = ymax - ymin;
+  }
+}
+
+__global__ void __launch_bounds__(NT, 1) k_conceal(KParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CellSmem& S = *reinterpret_cast<CellSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  double* gV = P.scratch + (size_t)blockIdx.x * P.scratch_per_cta;
+  double* gQ = gV + (size_t)MAXCAND * 32;
+  if (tid < 4) S.cnt[tid] = 0;
+  const int nslots = *((volatile int*)P.nslots);
+  for (;;) {
+    if (tid == 0) S.ticket = atomicAdd(P.ticket, 1u);
+    __syncthreads();
+    const int ticket = S.ticket;
+    if (ticket >= nslots) break;
+    if (tid == 0) {
+      const int slot = (int)P.order[ticket];
+      const int c = P.slot_cell[slot];
+      S.slot = slot;
+      S.f = c / (P.GR * P.GC);
+      const int rem = c % (P.GR * P.GC);
+      S.gr = rem / P.GC;
+      S.gc = rem % P.GC;
+    }
+    __syncthreads();
+    // wait for the earlier-raster lost 8-neighbours (profiles.py:298-302 order)
+    if (tid < 4) {
+      const int dr[4] = {-1, -1, -1, 0}, dc[4] = {-1, 0, 1, -1};
+      const int nr = S.gr + dr[tid], nc = S.gc + dc[tid];
+      if (nr >= 0 && nc >= 0 && nc < P.GC) {
+        const int ps = P.slotmap[((size_t)S.f * P.GR + nr) * P.GC + nc];
+        if (ps >= 0)
+          while (ld_acquire_u32(&P.done[ps]) == 0) __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    load_tile(P, S);
+    // lost_patch_origins (framework.py:219-227)
+    if (tid < 32) {
+      unsigned long long bits = 0;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int p = tid + 32 * h;
+        const int o = patch_r(p) * TS + patch_c(p);
+        const bool l = S.st[o] == ST_LO || S.st[o + 1] == ST_LO || S.st[o + TS] == ST_LO || S.st[o + TS + 1] == ST_LO;
+        const unsigned b = __ballot_sync(FULL, l);
+        bits |= (unsigned long long)b << (32 * h);
+      }
+      if (tid == 0) {
+        S.remaining = bits;
+        S.nrec = 0;
+      }
+    }
+    __syncthreads();
+    // _conceal_block (profiles.py:191-226)
+    while (S.remaining) {
+      if (tid == 0) {
+        S.ndef = 0;
+        S.progressed = 0;
+        S.pend = S.remaining;
+      }
+      __syncthreads();
+      while (S.pend) {
+        if (tid == 0) S.t_start = clock64();
+        if (tid < 32) pick_and_extract(S);
+        __syncthreads();
+        if (S.skip) {  // EmptyContextError -> deferred
+          if (tid == 0) S.deferred[S.ndef++] = S.pick;
+          __syncthreads();
+          continue;
+        }
+        estimate_patch(P, S, S.pick, gV, gQ);
+        if (tid == 0) S.progressed = 1;
+        __syncthreads();
+      }
+      if (S.ndef == 0) break;
+      if (S.progressed) {
+        __syncthreads();
+        if (tid == 0) {
+          unsigned long long b = 0;
+          for (int i = 0; i < S.ndef; i++) b |= 1ull << S.deferred[i];
+          S.remaining = b;
+        }
+        __syncthreads();
+      } else {
+        // 128 fill in deferral order (profiles.py:219-225)
+        if (tid == 0) {
+          for (int i = 0; i < S.ndef; i++) {
+            const int p = S.deferred[i];
+            const int pr_t = patch_r(p), pc_t = patch_c(p);
+            for (int q = 0; q < 4; q++) {
+              const int o = (pr_t + (q >> 1)) * TS + pc_t + (q & 1);
+              if (S.st[o] == ST_LO) {
+                S.tile[o] = 128.0;
+                S.tile32[o] = 128.f;
+                S.st[o] = ST_RE;
+              }
+            }
+            bm_patch_record rec;
+            memset(&rec, 0, sizeof(rec));
+            rec.frame = S.f;
+            rec.row = S.gr * BS - BS + pr_t;
+            rec.col = S.gc * BS - BS + pc_t;
+            rec.layer = BM_LAYER_NONE;
+            rec.flags = BM_REC_DEFERRED;
+            rec.m_candidates = -1;
+            rec.phi = rec.nu = rec.beta = rec.alpha = __longlong_as_double(0x7ff8000000000000ll);
+            rec.beta_gap = __int_as_float(0x7fc00000);
+            write_record(P, S, rec);
+            S.nrec++;
+            S.cnt[3]++;
+          }
+          S.remaining = 0;
+        }
+        __syncthreads();
+        break;
+      }
+    }
+    __syncthreads();
+    // publish the cell (values, outputs), then release the flag
+    {
+      const size_t slot = S.slot;
+      const int f = S.f;
+      const int r0 = S.gr * BS, c0 = S.gc * BS;
+      for (int i = tid; i < 256; i += NT) {
+        const int rr = i / BS, cc = i % BS;
+        const double v = S.tile[(BS + rr) * TS + BS + cc];
+        P.cellbuf[slot * 256 + i] = v;
+        const size_t o = ((size_t)f * P.H + r0 + rr) * P.W + c0 + cc;
+        if (P.out_f64) P.out_f64[o] = v;
+        if (P.out_u8) P.out_u8[o] = (uint8_t)floor(fmin(fmax(v, 0.0), 255.0) + 0.5);  // image.py:53-56
+      }
+      if (tid == 0 && P.records) P.rec_count[slot] = (uint8_t)S.nrec;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) st_release_u32(&P.done[slot], 1u);
+    }
+  }
+  __syncthreads();
+  if (tid < 4 && S.cnt[tid]) atomicAdd(&P.counters[tid], S.cnt[tid]);
+}
+
+// Dense output initialisation: out_f64 = pixels, out_u8 = quantized(pixels).
+__global__ void k_init_out(KParams P) {
+  const size_t n = (size_t)P.B * P.H * P.W;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const double v = P.pix_f64 ? ((const double*)P.pixels)[i] : (double)((const uint8_t*)P.pixels)[i];
+    if (P.out_f64) P.out_f64[i] = v;
+    if (P.out_u8) P.out_u8[i] = (uint8_t)floor(fmin(fmax(v, 0.0), 255.0) + 0.5);
+  }
+}
+
+__global__ void k_summary(KParams P, bm_summary* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    bm_summary s;
+    memset(&s, 0, sizeof(s));
+    s.lost_cells = *P.nslots;
+    for (int i = 0; i < 3; i++) s.layer_counts[i] = (int64_t)P.counters[i];
+    s.deferred_fills = (int64_t)P.counters[3];
+    s.patches = s.layer_counts[0] + s.layer_counts[1] + s.layer_counts[2] + s.deferred_fills;
+    s.lost_left = (int64_t)P.counters[4];
+    s.max_level = (int32_t)P.counters[7];
+    s.pad = (int32_t)P.counters[5];  // bad state values
+    *out = s;
+  }
+}
+
+// ------------------------------------------------------- dense estimator API
+
+struct EstBatchArgs {
+  int layer, count, max_m;
+  double sigma2;
+  const int32_t* n_y;
+  const int32_t* m;
+  const double* y0;
+  const double* x;
+  const double* y;
+  double* out_values;
+  bm_patch_record* out_info;
+  double* scratch;
+};
+
+struct EstBatchSmem {
+  float d2f[MAXCAND];
+  EstSmem est;
+};
+
+__global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  EstBatchSmem& S = *reinterpret_cast<EstBatchSmem*>(smem_raw);
+  EstSmem& E = S.est;
+  const int i = blockIdx.x, tid = threadIdx.x;
+  const int n = A.n_y[i], m = A.m[i];
+  const double* X = A.x + (size_t)i * A.max_m * 4;
+  const double* Y = A.y + (size_t)i * A.max_m * 32;
+  if (tid < 32) {
+    E.y0[tid] = tid < n ? A.y0[(size_t)i * 32 + tid] : 0.0;
+    E.y0f[tid] = (float)E.y0[tid];
+  }
+  if (tid == 0) E.n = n;
+  __syncthreads();
+  for (int j = tid; j < m; j += NT) {
+    float d2 = 0.f;
+    for (int k = 0; k < n; k++) {
+      const float d = (float)Y[(size_t)j * 32 + k] - E.y0f[k];
+      d2 = fmaf(d, d, d2);
+    }
+    S.d2f[j] = d2;
+  }
+  __syncthreads();
+  DenseAcc acc{X, Y};
+  double* gV = A.scratch + (size_t)blockIdx.x * ((size_t)MAXCAND * (32 + KMAX));
+  double* gQ = gV + (size_t)MAXCAND * 32;
+  bm_patch_record rec;
+  memset(&rec, 0, sizeof(rec));
+  rec.nu = rec.beta = rec.alpha = __longlong_as_double(0x7ff8000000000000ll);
+  rec.m_candidates = m;
+  rec.n_y = (uint8_t)n;
+  rec.flags = BM_REC_HAS_M;
+  int layer = BM_LAYER_BRL, fallback = 0;
+  bool done = false;
+  if (A.layer == BM_LAYER_HQL && m >= 2) {
+    hql_core(acc, m, E, gV, gQ);
+    if (E.ok) {
+      done = true;
+      layer = BM_LAYER_HQL;
+      rec.beta = E.beta;
+      rec.alpha = E.alpha;
+      rec.beta_gap = E.gap;
+      rec.flags |= BM_REC_HAS_BW;
+    }
+  }
+  if (!done && A.layer != BM_LAYER_BRL && m >= 1) {
+    idl_estimate_dev(acc, S.d2f, m, A.sigma2, E);
+    rec.nu = E.nu_raw;
+    rec.flags |= BM_REC_HAS_NU;
+    if (E.ok) {
+      done = true;
+      layer = BM_LAYER_IDL;
+      fallback = A.layer == BM_LAYER_HQL;
+    }
+  }
+  if (!done) {
+    brl_values(E);
+    fallback = A.layer != BM_LAYER_BRL;
+    if (A.layer != BM_LAYER_HQL) rec.m_candidates = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    rec.layer = (int8_t)layer;
+    if (fallback) rec.flags |= BM_REC_FALLBACK;
+    A.out_info[i] = rec;
+    for (int q = 0; q < 4; q++) A.out_values[(size_t)i * 4 + q] = E.vals[q];
+  }
+}
+
+__global__ void k_compact_records(const bm_patch_record* slot_rec, const uint8_t* cnt, const int* excl,
+                                  const int* nslots, bm_patch_record* out) {
+  const int ns = *nslots;
+  for (int s = blockIdx.x; s < ns; s += gridDim.x) {
+    const int c = cnt[s], base = excl[s];
+    for (int i = threadIdx.x; i < c; i += blockDim.x) out[base + i] = slot_rec[(size_t)s * 64 + i];
+  }
+}
+__global__ void k_u8_to_int(const uint8_t* c, const int* nslots, int* o, int n) {
+  const int ns = *nslots;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) o[i] = i < ns ? c[i] : 0;
+}
+
+}  // namespace bm
+
+// =================================================================== C ABI
+using namespace bm;
+
+namespace {
+
+struct Layout {
+  size_t ncell;
+  size_t off_slotmap, off_slot_cell, off_level, off_level2, off_order, off_order_in, off_done, off_nslots,
+      off_ticket, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_cub, cub_bytes, off_scratch,
+      scratch_per_cta, total;
+  int grid;
+};
+
+int g_sms = 0;
+int sm_count() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) g_sms = 148;
+  }
+  return g_sms;
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
+
+bool params_ok(const bm_params* p) {
+  return p && p->frames >= 1 && p->height >= 1 && p->width >= 1 && (p->pixel_dtype == BM_PIX_U8 || p->pixel_dtype == BM_PIX_F64) &&
+         p->forced_layer >= -1 && p->forced_layer <= 2 && p->sigma2 > 0.0;
+}
+
+Layout layout(const bm_params* p) {
+  Layout L;
+  memset(&L, 0, sizeof(L));
+  const size_t GR = p->height / BS, GC = p->width / BS;
+  L.ncell = (size_t)p->frames * GR * GC;
+  const size_t nc = L.ncell > 0 ? L.ncell : 1;
+  size_t o = 0;
+  L.off_slotmap = o; o = align_up(o + nc * 4);
+  L.off_slot_cell = o; o = align_up(o + nc * 4);
+  L.off_level = o; o = align_up(o + nc * 4);
+  L.off_level2 = o; o = align_up(o + nc * 4);
+  L.off_order = o; o = align_up(o + nc * 4);
+  L.off_order_in = o; o = align_up(o + nc * 4);
+  L.off_done = o; o = align_up(o + nc * 4);
+  L.off_nslots = o; o = align_up(o + 4);
+  L.off_ticket = o; o = align_up(o + 4);
+  L.off_flags = o; o = align_up(o + nc * 4);
+  L.off_excl = o; o = align_up(o + nc * 4);
+  L.off_cellbuf = o; o = align_up(o + nc * 256 * 8);
+  L.off_reccnt = o; o = align_up(o + nc);
+  L.off_counters = o; o = align_up(o + 8 * 8);
+  size_t b1 = 0, b2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, b1, (int*)nullptr, (int*)nullptr, (int)nc);
+  cub::DeviceRadixSort::SortPairs(nullptr, b2, (unsigned*)nullptr, (unsigned*)nullptr, (unsigned*)nullptr,
+                                  (unsigned*)nullptr, (int)nc);
+  L.cub_bytes = b1 > b2 ? b1 : b2;
+  L.off_cub = o; o = align_up(o + L.cub_bytes);
+  const int sms = sm_count();
+  L.grid = (int)(nc < (size_t)sms ? nc : (size_t)sms);
+  if (L.grid < 1) L.grid = 1;
+  L.scratch_per_cta = (size_t)MAXCAND * (32 + KMAX);
+  L.off_scratch = o; o = align_up(o + (size_t)L.grid * L.scratch_per_cta * 8);
+  L.total = o;
+  return L;
+}
+
+int cuda_status(cudaError_t e) {
+  if (e != cudaSuccess) {
+    fprintf(stderr, "blockmend_b200: CUDA error: %s\n", cudaGetErrorString(e));
+    return BM_ERR_CUDA;
+  }
+  return BM_OK;
+}
+
+bool g_attr_set = false;
+
+}  // namespace
+
+extern "C" {
+
+int bm_abi_version(void) { return BM_ABI_VERSION; }
+
+int bm_device_clock_khz(void) {
+  int dev = 0, khz = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, dev) != cudaSuccess) return 0;
+  return khz;
+}
+
+const char* bm_status_string(int s) {
+  switch (s) {
+    case BM_OK: return "ok";
+    case BM_ERR_ARGS: return "bad arguments or shape mismatch";
+    case BM_ERR_LOST_LEFT: return "concealment left LOST pixels behind";
+    case BM_ERR_CUDA: return "CUDA error or no CUDA device";
+    case BM_ERR_WORKSPACE: return "workspace too small";
+    case BM_ERR_STATES: return "mask contains a value outside the PixelState range";
+    default: return "unknown status";
+  }
+}
+
+size_t bm_workspace_bytes(const bm_params* p) {
+  if (!params_ok(p)) return 0;
+  return layout(p).total;
+}
+
+int64_t bm_max_records(const bm_params* p) {
+  if (!params_ok(p)) return 0;
+  return (int64_t)p->frames * (p->height / BS) * (p->width / BS) * 64;
+}
+
+int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, double* out_f64, uint8_t* out_u8,
+               bm_patch_record* out_records, bm_summary* out_summary, void* workspace, size_t workspace_bytes,
+               void* stream_) {
+  if (!params_ok(p) || !pixels || !states) return BM_ERR_ARGS;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  Layout L = layout(p);
+  if (!workspace || workspace_bytes < L.total) return BM_ERR_WORKSPACE;
+  char* ws = (char*)workspace;
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.B = p->frames;
+  P.H = p->height;
+  P.W = p->width;
+  P.GR = p->height / BS;
+  P.GC = p->width / BS;
+  P.pix_f64 = p->pixel_dtype == BM_PIX_F64;
+  P.t_phi = p->t_phi;
+  P.t_nu = p->t_nu;
+  P.sigma2 = p->sigma2;
+  P.forced = p->forced_layer;
+  P.pixels = pixels;
+  P.states = states;
+  P.out_f64 = out_f64;
+  P.out_u8 = out_u8;
+  P.records = out_records;
+  P.slotmap = (int*)(ws + L.off_slotmap);
+  P.slot_cell = (int*)(ws + L.off_slot_cell);
+  P.level = (unsigned*)(ws + L.off_level);
+  P.order = (unsigned*)(ws + L.off_order);
+  P.done = (unsigned*)(ws + L.off_done);
+  P.nslots = (int*)(ws + L.off_nslots);
+  P.ticket = (unsigned*)(ws + L.off_ticket);
+  P.cellbuf = (double*)(ws + L.off_cellbuf);
+  P.rec_count = (uint8_t*)(ws + L.off_reccnt);
+  P.counters = (unsigned long long*)(ws + L.off_counters);
+  P.scratch = (double*)(ws + L.off_scratch);
+  P.scratch_per_cta = L.scratch_per_cta;
+  int* flags = (int*)(ws + L.off_flags);
+  int* excl = (int*)(ws + L.off_excl);
+  const int nc = (int)L.ncell;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(P.counters, 0, 64, stream)) != cudaSuccess) return cuda_status(e);
+  if ((e = cudaMemsetAsync(P.ticket, 0, 4, stream)) != cudaSuccess) return cuda_status(e);
+  if (nc == 0) {
+    if ((e = cudaMemsetAsync(P.nslots, 0, 4, stream)) != cudaSuccess) return cuda_status(e);
+  }
+  const int sms = sm_count();
+  // dense outputs first (non-lost cells keep their input values)
+  if (out_f64 || out_u8) k_init_out<<<sms * 4, 256, 0, stream>>>(P);
+  if (nc > 0) {
+    k_cell_flags<<<sms * 4, 256, 0, stream>>>(P, flags);
+    size_t cb = L.cub_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cb, flags, excl, nc, stream)) != cudaSuccess)
+      return cuda_status(e);
+    k_slots<<<sms * 4, 256, 0, stream>>>(P, flags, excl);
+    // invalid slots (>= nslots) keep the max key so they sort last
+    if ((e = cudaMemsetAsync(P.level, 0xff, (size_t)nc * 4, stream)) != cudaSuccess) return cuda_status(e);
+    k_levels<<<(P.B + 7) / 8, 256, 0, stream>>>(P);
+    // ticket order: slots sorted by level (stable -> frame, raster within a level)
+    k_iota<<<sms, 256, 0, stream>>>((unsigned*)(ws + L.off_order_in), P.nslots, nc);
+    // slots beyond nslots carry garbage levels: give them the max key
+    cb = L.cub_bytes;
+    if ((e = cub::DeviceRadixSort::SortPairs(ws + L.off_cub, cb, P.level, (unsigned*)(ws + L.off_level2),
+                                             (unsigned*)(ws + L.off_order_in), P.order, nc, 0, 32, stream)) !=
+        cudaSuccess)
+      return cuda_status(e);
+    const size_t smem = sizeof(CellSmem);
+    if (!g_attr_set) {
+      if ((e = cudaFuncSetAttribute(k_conceal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return cuda_status(e);
+      g_attr_set = true;
+    }
+    k_conceal<<<L.grid, NT, smem, stream>>>(P);
+  }
+  if (out_summary) k_summary<<<1, 32, 0, stream>>>(P, out_summary);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_status(e);
+  return BM_OK;
+}
+
+int bm_compact_records(const bm_params* p, const bm_patch_record* slot_records, void* workspace,
+                       bm_patch_record* out_records, int64_t* out_count, void* stream_) {
+  if (!params_ok(p) || !slot_records || !workspace || !out_records || !out_count) return BM_ERR_ARGS;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  Layout L = layout(p);
+  char* ws = (char*)workspace;
+  const int nc = (int)L.ncell;
+  if (nc == 0) {
+    *out_count = 0;
+    return BM_OK;
+  }
+  int* cnt = (int*)(ws + L.off_flags);  // flags are dead after bm_conceal
+  int* excl = (int*)(ws + L.off_level2);
+  k_u8_to_int<<<sm_count(), 256, 0, stream>>>((const uint8_t*)(ws + L.off_reccnt), (int*)(ws + L.off_nslots), cnt, nc);
+  size_t cb = L.cub_bytes;
+  cudaError_t e;
+  if ((e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cb, cnt, excl, nc, stream)) != cudaSuccess)
+    return cuda_status(e);
+  k_compact_records<<<sm_count() * 4, 64, 0, stream>>>(slot_records, (const uint8_t*)(ws + L.off_reccnt), excl,
+                                                        (int*)(ws + L.off_nslots), out_records);
+  int last_excl = 0, last_cnt = 0;
+  if ((e = cudaMemcpyAsync(&last_excl, excl + nc - 1, 4, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+    return cuda_status(e);
+  if ((e = cudaMemcpyAsync(&last_cnt, cnt + nc - 1, 4, cudaMemcpyDeviceToHost, stream)) != cudaSuccess)
+    return cuda_status(e);
+  if ((e = cudaStreamSynchronize(stream)) != cudaSuccess) return cuda_status(e);
+  *out_count = (int64_t)last_excl + last_cnt;
+  return BM_OK;
+}
+
+int bm_estimate_batch(int32_t layer, int32_t count, int32_t max_m, double sigma2, const int32_t* n_y,
+                      const int32_t* m, const double* y0, const double* x, const double* y, double* out_values,
+                      bm_patch_record* out_info, void* stream_) {
+  if (count < 0 || max_m < 0 || max_m > MAXCAND || layer < 0 || layer > 2 || !(sigma2 > 0.0)) return BM_ERR_ARGS;
+  if (count == 0) return BM_OK;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  cudaError_t e;
+  double* scratch = nullptr;
+  const size_t per = (size_t)MAXCAND * (32 + KMAX);
+  if ((e = cudaMallocAsync((void**)&scratch, (size_t)count * per * 8, stream)) != cudaSuccess) return cuda_status(e);
+  EstBatchArgs A{layer, count, max_m, sigma2, n_y, m, y0, x, y, out_values, out_info, scratch};
+  const size_t smem = sizeof(EstBatchSmem);
+  static bool attr = false;
+  if (!attr) {
+    if ((e = cudaFuncSetAttribute(k_estimate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return cuda_status(e);
+    attr = true;
+  }
+  k_estimate_batch<<<count, NT, smem, stream>>>(A);
+  if ((e = cudaGetLastError()) != cudaSuccess) return cuda_status(e);
+  cudaFreeAsync(scratch, stream);
+  return BM_OK;
+}
+
+// Host-buffer entry: cached device buffers per shape, pinned staging.
+namespace {
+std::mutex g_host_mu;
+struct HostCache {
+  size_t npix = 0, pixbytes = 0, ws_bytes = 0, rec_cap = 0;
+  void *d_pix = nullptr, *d_ws = nullptr;
+  uint8_t *d_st = nullptr, *d_u8 = nullptr;
+  double* d_f64 = nullptr;
+  bm_patch_record *d_rec = nullptr, *d_rec2 = nullptr;
+  bm_summary* d_sum = nullptr;
+  cudaStream_t stream = nullptr;
+};
+HostCache g_host;
+}  // namespace
+
+int bm_conceal_host(const bm_params* p, const void* pixels, const uint8_t* states, double* out_f64, uint8_t* out_u8,
+                    bm_patch_record* out_records, int64_t* out_nrec, bm_summary* out_summary) {
+  if (!params_ok(p) || !pixels || !states) return BM_ERR_ARGS;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  HostCache& C = g_host;
+  cudaError_t e;
+  if (!C.stream && (e = cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return cuda_status(e);
+  const size_t npix = (size_t)p->frames * p->height * p->width;
+  const size_t pixbytes = npix * (p->pixel_dtype == BM_PIX_F64 ? 8 : 1);
+  const size_t wsb = bm_workspace_bytes(p);
+  const size_t rec_cap = out_records ? (size_t)bm_max_records(p) : 0;
+  if (npix != C.npix || pixbytes != C.pixbytes || wsb > C.ws_bytes || rec_cap > C.rec_cap) {
+    cudaFree(C.d_pix); cudaFree(C.d_ws); cudaFree(C.d_st); cudaFree(C.d_u8); cudaFree(C.d_f64);
+    cudaFree(C.d_rec); cudaFree(C.d_rec2); cudaFree(C.d_sum);
+    C = HostCache{};
+    if ((e = cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaMalloc(&C.d_pix, pixbytes)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaMalloc((void**)&C.d_st, npix)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaMalloc((void**)&C.d_u8, npix)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaMalloc((void**)&C.d_f64, npix * 8)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaMalloc(&C.d_ws, wsb)) != cudaSuccess) return cuda_status(e);
+    if ((e = cudaMalloc((void**)&C.d_sum, sizeof(bm_summary))) != cudaSuccess) return cuda_status(e);
+    if (rec_cap) {
+      if ((e = cudaMalloc((void**)&C.d_rec, rec_cap * sizeof(bm_patch_record))) != cudaSuccess) return cuda_status(e);
+      if ((e = cudaMalloc((void**)&C.d_rec2, rec_cap * sizeof(bm_patch_record))) != cudaSuccess) return cuda_status(e);
+    }
+    C.npix = npix;
+    C.pixbytes = pixbytes;
+    C.ws_bytes = wsb;
+    C.rec_cap = rec_cap;
+  }
+  if ((e = cudaMemcpyAsync(C.d_pix, pixels, pixbytes, cudaMemcpyHostToDevice, C.stream)) != cudaSuccess)
+    return cuda_status(e);
+  if ((e = cudaMemcpyAsync(C.d_st, states, npix, cudaMemcpyHostToDevice, C.stream)) != cudaSuccess)
+    return cuda_status(e);
+  int rc = bm_conceal(p, C.d_pix, C.d_st, out_f64 ? C.d_f64 : nullptr, C.d_u8, out_records ? C.d_rec : nullptr,
+                      C.d_sum, C.d_ws, C.ws_bytes, C.stream);
+  if (rc) return rc;
+  bm_summary sum;
+  if ((e = cudaMemcpyAsync(&sum, C.d_sum, sizeof(sum), cudaMemcpyDeviceToHost, C.stream)) != cudaSuccess)
+    return cuda_status(e);
+  if (out_u8 && (e = cudaMemcpyAsync(out_u8, C.d_u8, npix, cudaMemcpyDeviceToHost, C.stream)) != cudaSuccess)
+    return cuda_status(e);
+  if (out_f64 && (e = cudaMemcpyAsync(out_f64, C.d_f64, npix * 8, cudaMemcpyDeviceToHost, C.stream)) != cudaSuccess)
+    return cuda_status(e);
+  if (out_records) {
+    int64_t cnt = 0;
+    rc = bm_compact_records(p, C.d_rec, C.d_ws, C.d_rec2, &cnt, C.stream);
+    if (rc) return rc;
+    if (cnt > 0 && (e = cudaMemcpyAsync(out_records, C.d_rec2, (size_t)cnt * sizeof(bm_patch_record),
+                                        cudaMemcpyDeviceToHost, C.stream)) != cudaSuccess)
+      return cuda_status(e);
+    if (out_nrec) *out_nrec = cnt;
+  }
+  if ((e = cudaStreamSynchronize(C.stream)) != cudaSuccess) return cuda_status(e);
+  if (out_summary) *out_summary = sum;
+  if (sum.pad) return BM_ERR_STATES;
+  if (sum.lost_left) return BM_ERR_LOST_LEFT;
+  return BM_OK;
+}
+
+}  // extern "C"
