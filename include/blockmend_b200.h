@@ -94,8 +94,16 @@ typedef struct bm_summary {
   int64_t deferred_fills;
   int64_t lost_left;      /* LOST pixels outside the block grid (must be 0) */
   int32_t max_level;      /* depth of the cross-cell dependency DAG */
-  int32_t pad;
+  int32_t bad_states;     /* cells/pixels with a state value > 2 */
+  /* algorithmic work (SURVEY.md §8(d) formulas, counted per patch) */
+  int64_t flop64;         /* FP64: HQL pipeline + IDL estimate */
+  int64_t flop32;         /* FP32: nu-gate distance/weight screening */
+  int64_t hql_patches;    /* patches that ran the full HQL pipeline */
+  int64_t gate_candidates;/* candidates screened by the FP32 nu gate */
 } bm_summary;
+
+/* bm_params.flags */
+#define BM_FLAG_TIME_KERNEL 1 /* time the concealment kernel with CUDA events (bm_last_kernel_ms) */
 
 /* ---- queries ---- */
 int bm_abi_version(void);
@@ -104,6 +112,11 @@ const char* bm_status_string(int status);
 size_t bm_workspace_bytes(const bm_params* p);
 /* upper bound on records (64 per 16x16 cell of the grid) */
 int64_t bm_max_records(const bm_params* p);
+/* Durations (ms) of the concealment kernels launched with BM_FLAG_TIME_KERNEL
+ * since the last reset (CUDA events recorded on the launch stream around each
+ * launch; up to 256 kept).  Synchronises on the events.  Returns the count. */
+int bm_kernel_times_ms(float* out, int cap);
+void bm_kernel_times_reset(void);
 /* SM clock of the current device in kHz (converts bm_patch_record.cycles to
  * seconds for ConcealmentReport.patch_times); 0 when no device. */
 int bm_device_clock_khz(void);

@@ -25,6 +25,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
 ]
 
+BM_FLAG_TIME_KERNEL = 1
 BM_OK, BM_ERR_ARGS, BM_ERR_LOST_LEFT, BM_ERR_CUDA, BM_ERR_WORKSPACE, BM_ERR_STATES = 0, 1, 2, 3, 4, 5
 
 
@@ -50,13 +51,18 @@ class Summary(ctypes.Structure):
         ("deferred_fills", ctypes.c_int64),
         ("lost_left", ctypes.c_int64),
         ("max_level", ctypes.c_int32),
-        ("pad", ctypes.c_int32),
+        ("bad_states", ctypes.c_int32),
+        ("flop64", ctypes.c_int64),
+        ("flop32", ctypes.c_int64),
+        ("hql_patches", ctypes.c_int64),
+        ("gate_candidates", ctypes.c_int64),
     ]
 
 
 SUMMARY_BYTES = ctypes.sizeof(Summary)
 EXPORTS = [
     "bm_abi_version", "bm_status_string", "bm_workspace_bytes", "bm_max_records", "bm_device_clock_khz",
+    "bm_kernel_times_ms", "bm_kernel_times_reset",
     "bm_conceal", "bm_compact_records", "bm_conceal_host", "bm_estimate_batch",
 ]
 
@@ -104,6 +110,9 @@ def lib():
     L.bm_max_records.restype = i64
     L.bm_max_records.argtypes = [ctypes.POINTER(Params)]
     L.bm_device_clock_khz.restype = ctypes.c_int
+    L.bm_kernel_times_ms.restype = ctypes.c_int
+    L.bm_kernel_times_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
+    L.bm_kernel_times_reset.restype = None
     L.bm_conceal.restype = ctypes.c_int
     L.bm_conceal.argtypes = [ctypes.POINTER(Params), vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.bm_compact_records.restype = ctypes.c_int
@@ -136,3 +145,14 @@ def require_cuda():
     if not torch.cuda.is_available():
         raise NativeUnavailableError("no CUDA device: the B200 path has no CPU fallback")
     return torch
+
+
+def kernel_times_ms() -> list[float]:
+    """Durations of the timed concealment-kernel launches since the last reset."""
+    buf = (ctypes.c_float * 256)()
+    n = lib().bm_kernel_times_ms(buf, 256)
+    return [float(buf[i]) for i in range(n)]
+
+
+def kernel_times_reset() -> None:
+    lib().bm_kernel_times_reset()

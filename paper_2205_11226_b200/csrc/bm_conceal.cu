@@ -52,7 +52,8 @@ struct KParams {
   unsigned* ticket;    // [1]
   double* cellbuf;     // [ncell][256]
   uint8_t* rec_count;  // [ncell]
-  unsigned long long* counters;  // [8]: BRL, IDL, HQL, deferred, lost_left, bad_states, patches, maxlevel
+  unsigned long long* counters;  // [12]: BRL, IDL, HQL, deferred, lost_left, bad_states, -, maxlevel,
+                                 //       flop64, flop32, hql_patches, gate_candidates
   double* scratch;     // per-CTA HQL scratch
   size_t scratch_per_cta;  // doubles
 };
@@ -63,7 +64,6 @@ struct CellSmem {
   uint64_t lostbits[TILE];
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
-  float d2f[MAXCAND];
   float rbuf[NT];
   int pref[NT];
   int wcnt[NWARP];
@@ -78,7 +78,7 @@ struct CellSmem {
   double nu, carry, phi;
   unsigned rowmask[6];
   long long t_start;
-  unsigned long long cnt[4];
+  unsigned long long cnt[8];  // BRL IDL HQL deferred | flop64 flop32 hql gate
   EstSmem est;
 };
 
@@ -264,7 +264,7 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
 // Gather of the admissible candidates in (ring, row, col) order with the ring
 // by ring nu gate (profiles.py:113-124, framework.py:171-207), or the one-shot
 // full gather of _forced_estimate (profiles.py:148-149).  Sets S.m, rings_used,
-// nu; S.cand / S.d2f hold the candidates.
+// nu; S.cand holds the candidates.
 __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool gated) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
@@ -321,7 +321,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   for (int e0 = 0; e0 < K; e0 += NT) {
     const int e = e0 + tid;
     bool adm = false;
-    float d2 = 0.f, rw = 0.f;
+    float rw = 0.f;
     int pos = 0;
     if (e < K) {
       int r = 1;
@@ -335,12 +335,17 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
         if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) adm = false;
       if (adm) {
         pos = wr * TS + wc;
-        const float* tp = S.tile32 + pos;
-        for (int k = 0; k < n; k++) {
-          const float d = tp[E.uoff[k]] - E.y0f[k];
-          d2 = fmaf(d, d, d2);
+        if (gated) {
+          // nu screening: FP32 Nadaraya-Watson distance + weight
+          // (raw_idl_weights, estimators.py:105-109)
+          const float* tp = S.tile32 + pos;
+          float d2 = 0.f;
+          for (int k = 0; k < n; k++) {
+            const float d = tp[E.uoff[k]] - E.y0f[k];
+            d2 = fmaf(d, d, d2);
+          }
+          rw = expf(-d2 * invf);
         }
-        if (gated) rw = expf(-d2 * invf);  // raw_idl_weights (estimators.py:105-109)
       }
     }
     // ordered compaction
@@ -356,10 +361,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
       tot += S.wcnt[w];
     }
     const int m0 = S.m_total;
-    if (adm) {
-      S.cand[m0 + base + wpre] = (uint16_t)pos;
-      S.d2f[m0 + base + wpre] = d2;
-    }
+    if (adm) S.cand[m0 + base + wpre] = (uint16_t)pos;
     S.pref[tid] = base + wpre + (adm ? 1 : 0);  // inclusive count up to e
     __syncthreads();
     if (!gated) {
@@ -413,6 +415,20 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   __syncthreads();
 }
 
+// Algorithmic FLOPs of one patch; exps are SFU work, not counted.
+__device__ __forceinline__ unsigned long long idl_flops(long long M, long long n) { return (unsigned long long)(M * (3 * n + 15)); }
+__device__ __forceinline__ unsigned long long hql_flops(long long M, long long n) {
+  const long long G = NBETA, k = min(n + 1, M);
+  long long f = 2 * M * (4 * n + n * (n + 1) / 2) + 2 * M * (n + 4);  // covariance (+ centring)
+  f += n * n * n / 3;                                                 // Cholesky
+  f += M * (n * n + 3 * n);                                           // quadforms
+  f += G * (M * (2 * n + 4) + 3 * n);                                 // beta grid
+  f += 2 * M * (n + 4);                                               // x~0, y~0
+  f += M * (n * n + 2 * n) + 2 * k * M * n + 2 * k * M * (n + 4) + 2 * k * n * n + 8 * n * k;  // alpha
+  f += 2 * n * n + 8 * n;                                             // correction
+  return (unsigned long long)f;
+}
+
 __device__ void write_record(const KParams& P, CellSmem& S, const bm_patch_record& rec) {
   if (P.records) P.records[(size_t)S.slot * 64 + S.nrec] = rec;
 }
@@ -448,6 +464,11 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV,
     const bool gated = forced < 0;
     gather(P, S, pr_t, pc_t, gated);
     const int m = S.m;
+    if (tid == 0 && gated) {
+      // nu loop: M_g (3n + 2) FP32 flops; exps counted separately
+      S.cnt[5] += (unsigned long long)m * (3 * E.n + 2);
+      S.cnt[7] += (unsigned long long)m;
+    }
     TileAcc acc{S.tile, S.cand, E.uoff};
     if (tid == 0) {
       rec.rings_used = (uint8_t)S.rings_used;
@@ -455,17 +476,19 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV,
     }
     if (gated && !(S.nu < P.t_nu)) {
       // nu >= T_nu -> IDL (profiles.py:123-124); nu > 0 so no underflow
-      idl_estimate_dev(acc, S.d2f, m, P.sigma2, E);
+      idl_estimate_dev(acc, m, P.sigma2, E);
       if (tid == 0) {
         rec.layer = BM_LAYER_IDL;
         rec.nu = S.nu;
         rec.flags |= BM_REC_HAS_NU;
+        S.cnt[4] += idl_flops(m, E.n);
       }
     } else if (forced == BM_LAYER_IDL) {  // profiles.py:144-153
       bool ok = false;
       if (m >= 1) {
-        idl_estimate_dev(acc, S.d2f, m, P.sigma2, E);
+        idl_estimate_dev(acc, m, P.sigma2, E);
         ok = E.ok;
+        if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
       }
       if (ok) {
         if (tid == 0) {
@@ -489,6 +512,8 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV,
         if (E.ok) {
           done = true;
           if (tid == 0) {
+            S.cnt[4] += hql_flops(m, E.n);
+            S.cnt[6]++;
             rec.layer = BM_LAYER_HQL;
             rec.beta = E.beta;
             rec.alpha = E.alpha;
@@ -498,7 +523,8 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV,
         }
       }
       if (!done && m >= 1) {
-        idl_estimate_dev(acc, S.d2f, m, P.sigma2, E);
+        idl_estimate_dev(acc, m, P.sigma2, E);
+        if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
         if (E.ok) {
           done = true;
           if (tid == 0) {
@@ -618,7 +644,7 @@ __global__ void __launch_bounds__(NT, 1) k_conceal(KParams P) {
   const int tid = threadIdx.x;
   double* gV = P.scratch + (size_t)blockIdx.x * P.scratch_per_cta;
   double* gQ = gV + (size_t)MAXCAND * 32;
-  if (tid < 4) S.cnt[tid] = 0;
+  if (tid < 8) S.cnt[tid] = 0;
   const int nslots = *((volatile int*)P.nslots);
   for (;;) {
     if (tid == 0) S.ticket = atomicAdd(P.ticket, 1u);
@@ -750,6 +776,7 @@ __global__ void __launch_bounds__(NT, 1) k_conceal(KParams P) {
   }
   __syncthreads();
   if (tid < 4 && S.cnt[tid]) atomicAdd(&P.counters[tid], S.cnt[tid]);
+  if (tid >= 4 && tid < 8 && S.cnt[tid]) atomicAdd(&P.counters[tid + 4], S.cnt[tid]);
 }
 
 // Dense output initialisation: out_f64 = pixels, out_u8 = quantized(pixels).
@@ -772,7 +799,11 @@ __global__ void k_summary(KParams P, bm_summary* out) {
     s.patches = s.layer_counts[0] + s.layer_counts[1] + s.layer_counts[2] + s.deferred_fills;
     s.lost_left = (int64_t)P.counters[4];
     s.max_level = (int32_t)P.counters[7];
-    s.pad = (int32_t)P.counters[5];  // bad state values
+    s.bad_states = (int32_t)P.counters[5];
+    s.flop64 = (int64_t)P.counters[8];
+    s.flop32 = (int64_t)P.counters[9];
+    s.hql_patches = (int64_t)P.counters[10];
+    s.gate_candidates = (int64_t)P.counters[11];
     *out = s;
   }
 }
@@ -793,7 +824,6 @@ struct EstBatchArgs {
 };
 
 struct EstBatchSmem {
-  float d2f[MAXCAND];
   EstSmem est;
 };
 
@@ -810,15 +840,6 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
     E.y0f[tid] = (float)E.y0[tid];
   }
   if (tid == 0) E.n = n;
-  __syncthreads();
-  for (int j = tid; j < m; j += NT) {
-    float d2 = 0.f;
-    for (int k = 0; k < n; k++) {
-      const float d = (float)Y[(size_t)j * 32 + k] - E.y0f[k];
-      d2 = fmaf(d, d, d2);
-    }
-    S.d2f[j] = d2;
-  }
   __syncthreads();
   DenseAcc acc{X, Y};
   double* gV = A.scratch + (size_t)blockIdx.x * ((size_t)MAXCAND * (32 + KMAX));
@@ -843,7 +864,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
     }
   }
   if (!done && A.layer != BM_LAYER_BRL && m >= 1) {
-    idl_estimate_dev(acc, S.d2f, m, A.sigma2, E);
+    idl_estimate_dev(acc, m, A.sigma2, E);
     rec.nu = E.nu_raw;
     rec.flags |= BM_REC_HAS_NU;
     if (E.ok) {
@@ -931,7 +952,7 @@ Layout layout(const bm_params* p) {
   L.off_excl = o; o = align_up(o + nc * 4);
   L.off_cellbuf = o; o = align_up(o + nc * 256 * 8);
   L.off_reccnt = o; o = align_up(o + nc);
-  L.off_counters = o; o = align_up(o + 8 * 8);
+  L.off_counters = o; o = align_up(o + 16 * 8);
   size_t b1 = 0, b2 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b1, (int*)nullptr, (int*)nullptr, (int)nc);
   cub::DeviceRadixSort::SortPairs(nullptr, b2, (unsigned*)nullptr, (unsigned*)nullptr, (unsigned*)nullptr,
@@ -956,12 +977,29 @@ int cuda_status(cudaError_t e) {
 }
 
 bool g_attr_set = false;
+constexpr int NEV = 256;
+cudaEvent_t g_ev[NEV][2];
+bool g_ev_init = false;
+int g_nev = 0;
 
 }  // namespace
 
 extern "C" {
 
 int bm_abi_version(void) { return BM_ABI_VERSION; }
+
+int bm_kernel_times_ms(float* out, int cap) {
+  int n = g_nev < cap ? g_nev : cap;
+  for (int i = 0; i < n; i++) {
+    float ms = -1.f;
+    if (cudaEventSynchronize(g_ev[i][1]) != cudaSuccess) return i;
+    cudaEventElapsedTime(&ms, g_ev[i][0], g_ev[i][1]);
+    out[i] = ms;
+  }
+  return n;
+}
+
+void bm_kernel_times_reset(void) { g_nev = 0; }
 
 int bm_device_clock_khz(void) {
   int dev = 0, khz = 0;
@@ -1033,7 +1071,7 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   int* excl = (int*)(ws + L.off_excl);
   const int nc = (int)L.ncell;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(P.counters, 0, 64, stream)) != cudaSuccess) return cuda_status(e);
+  if ((e = cudaMemsetAsync(P.counters, 0, 16 * 8, stream)) != cudaSuccess) return cuda_status(e);
   if ((e = cudaMemsetAsync(P.ticket, 0, 4, stream)) != cudaSuccess) return cuda_status(e);
   if (nc == 0) {
     if ((e = cudaMemsetAsync(P.nslots, 0, 4, stream)) != cudaSuccess) return cuda_status(e);
@@ -1064,7 +1102,23 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
         return cuda_status(e);
       g_attr_set = true;
     }
+    const bool timed = (p->flags & BM_FLAG_TIME_KERNEL) != 0;
+    const int slot_ev = g_nev < NEV ? g_nev : NEV - 1;
+    if (timed) {
+      if (!g_ev_init) {
+        for (int i = 0; i < NEV; i++) {
+          cudaEventCreate(&g_ev[i][0]);
+          cudaEventCreate(&g_ev[i][1]);
+        }
+        g_ev_init = true;
+      }
+      cudaEventRecord(g_ev[slot_ev][0], stream);
+    }
     k_conceal<<<L.grid, NT, smem, stream>>>(P);
+    if (timed) {
+      cudaEventRecord(g_ev[slot_ev][1], stream);
+      if (g_nev < NEV) g_nev++;
+    }
   }
   if (out_summary) k_summary<<<1, 32, 0, stream>>>(P, out_summary);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_status(e);
@@ -1198,7 +1252,7 @@ int bm_conceal_host(const bm_params* p, const void* pixels, const uint8_t* state
   }
   if ((e = cudaStreamSynchronize(C.stream)) != cudaSuccess) return cuda_status(e);
   if (out_summary) *out_summary = sum;
-  if (sum.pad) return BM_ERR_STATES;
+  if (sum.bad_states) return BM_ERR_STATES;
   if (sum.lost_left) return BM_ERR_LOST_LEFT;
   return BM_OK;
 }

@@ -134,36 +134,76 @@ __device__ __forceinline__ void brl_values(EstSmem& S) {
   }
 }
 
-// ----------------------------------------------------------------------- IDL
-// idl_weights / idl_estimate (estimators.py:112-132) over m candidates whose
-// FP32 squared context distances d2f[] are precomputed (gather stage).
-// Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0).  S.nu_raw = raw_sum.
-template <class Acc>
-__device__ void idl_estimate_dev(const Acc& acc, const float* d2f, int m, double sigma2, EstSmem& S) {
-  const int n = S.n;
-  float dmin = FLT_MAX;
-  for (int j = threadIdx.x; j < m; j += NT) dmin = fminf(dmin, d2f[j]);
-  dmin = cta_minf(dmin, S);
-  const double c64 = 2.0 * sigma2 * n;
-  const float invf = (float)(1.0 / c64);
-  double v[32];
-  double xs[5] = {0, 0, 0, 0, 0};
+// Pairwise (NumPy) sum of v[i]^2 for i < n with v in registers.
+__device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
+  if (n < 8) {
+    double res = 0.0;
 #pragma unroll
-  for (int i = 0; i < 32; i++) v[i] = 0.0;
+    for (int i = 0; i < 8; i++)
+      if (i < n) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
+    return res;
+  }
+  const int n8 = n - (n % 8);
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) r[j] = __dmul_rn(v[j], v[j]);
+#pragma unroll
+  for (int i = 8; i < 32; i++)
+    if (i < n8) r[i & 7] = __dadd_rn(r[i & 7], __dmul_rn(v[i], v[i]));
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+#pragma unroll
+  for (int i = 8; i < 32; i++)
+    if (i >= n8 && i < n) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
+  return res;
+}
+
+// ----------------------------------------------------------------------- IDL
+// idl_weights / idl_estimate (estimators.py:112-132) in FP64, mirroring the
+// reference's arithmetic: d2 in NumPy's pairwise order, expo = -d2/(2 s2 N_y),
+// w = exp(expo - max) / sum, values = w @ x.  (The FP32 Nadaraya-Watson
+// distance/weight work is the nu gate's screening pass in gather(); FP32 in
+// the *estimate* itself is amplified ~1e4x along the patch chain and breaks
+// the +-1 LSB bar.)
+// Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
+template <class Acc>
+__device__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S) {
+  const int n = S.n;
+  const double c = 2.0 * sigma2 * n;
+  double emax = -INFINITY;
   for (int j = threadIdx.x; j < m; j += NT) {
-    const double w = (double)expf((dmin - d2f[j]) * invf);
-    xs[0] += w;
+    double v[32];
+#pragma unroll
+    for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
+    const double expo = -pairwise_sq32(v, n) / c;
+    S.dq[j] = expo;
+    emax = fmax(emax, expo);
+  }
+  emax = -cta_min(-emax, S);
+  double xs[5] = {0, 0, 0, 0, 0};
+  double vz[32];
+#pragma unroll
+  for (int t = 0; t < 32; t++) vz[t] = 0.0;
+  for (int j = threadIdx.x; j < m; j += NT) {
+    const double sh = exp(S.dq[j] - emax);
+    S.e2[j] = sh;
+    xs[0] += sh;
+  }
+  cta_sum40<1>(vz, *reinterpret_cast<double(*)[1]>(xs), S.P[0], S);
+  const double tot = S.P[0][32];
+  xs[0] = 0.0;
+  for (int j = threadIdx.x; j < m; j += NT) {
+    const double w = S.e2[j] / tot;
 #pragma unroll
     for (int q = 0; q < 4; q++) xs[1 + q] = fma(w, acc.x(j, q), xs[1 + q]);
   }
-  cta_sum40<5>(v, xs, S.P[0], S);
+#pragma unroll
+  for (int t = 0; t < 32; t++) vz[t] = 0.0;
+  cta_sum40<5>(vz, xs, S.P[1], S);
   if (threadIdx.x == 0) {
-    const double tot = S.P[0][32];
-    // raw_sum = sum exp(expo_j); exactly 0.0 in FP64 iff exp(max expo) == 0.0
-    const double emax = exp(-(double)dmin / c64);
-    S.nu_raw = emax * tot;
-    S.ok = emax != 0.0;
-    for (int q = 0; q < 4; q++) S.vals[q] = S.P[0][33 + q] / tot;
+    const double e0 = exp(emax);  // raw_sum == 0.0 iff the largest term underflows
+    S.nu_raw = e0 * tot;
+    S.ok = e0 != 0.0;
+    for (int q = 0; q < 4; q++) S.vals[q] = S.P[1][33 + q];
   }
   __syncthreads();
 }
@@ -189,29 +229,6 @@ __device__ __forceinline__ void bwd_solve32(const double* L, const double* rdiag
     for (int k = t + 1; k < 32; k++) s = fma(-L[k * 33 + t], v[k], s);
     v[t] = s * rdiag[t];
   }
-}
-
-// Pairwise (NumPy) sum of v[i]^2 for i < n with v in registers.
-__device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
-  if (n < 8) {
-    double res = 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; i++)
-      if (i < n) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
-    return res;
-  }
-  const int n8 = n - (n % 8);
-  double r[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++) r[j] = __dmul_rn(v[j], v[j]);
-#pragma unroll
-  for (int i = 8; i < 32; i++)
-    if (i < n8) r[i & 7] = __dadd_rn(r[i & 7], __dmul_rn(v[i], v[i]));
-  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-#pragma unroll
-  for (int i = 8; i < 32; i++)
-    if (i >= n8 && i < n) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
-  return res;
 }
 
 // Full HQL pipeline (estimators.py:256-273).  Returns via S: ok (0 -> the

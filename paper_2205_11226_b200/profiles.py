@@ -172,6 +172,7 @@ def conceal_batch(
     records: bool = False,
     out_u8=None,
     sync: bool = True,
+    time_kernel: bool = False,
 ) -> BatchResult:
     """Conceal B frames resident on the GPU.
 
@@ -201,6 +202,8 @@ def conceal_batch(
     states = states.to(torch.uint8).contiguous()
     b, h, w = frames.shape
     params = make_params(b, h, w, pix_dtype, profile, sigma2, forced_layer)
+    if time_kernel:
+        params.flags |= _native.BM_FLAG_TIME_KERNEL
     dev = frames.device
     nbytes = _WS.get(torch, params, dev, records)
     u8 = None
@@ -228,9 +231,13 @@ def conceal_batch(
             "deferred_fills": int(s.deferred_fills),
             "lost_left": int(s.lost_left),
             "max_level": int(s.max_level),
-            "bad_states": int(s.pad),
+            "bad_states": int(s.bad_states),
+            "flop64": int(s.flop64),
+            "flop32": int(s.flop32),
+            "hql_patches": int(s.hql_patches),
+            "gate_candidates": int(s.gate_candidates),
         }
-        if s.pad:
+        if s.bad_states:
             _native.check(_native.BM_ERR_STATES)
         if s.lost_left:
             _native.check(_native.BM_ERR_LOST_LEFT)

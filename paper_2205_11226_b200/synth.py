@@ -118,19 +118,20 @@ CONFIGS = {
 }
 
 
-def make_config(cfg: int, frames: int | None = None, crop: tuple[int, int] | None = None):
-    """Frames [B,h,w] u8 and states [B,h,w] u8 of BASELINE config `cfg`.
+def make_config(cfg: int, frames: int | None = None, crop: tuple[int, int] | None = None, first: int = 0):
+    """Frames [first, first+B) of BASELINE config `cfg`: u8 pixels and states [B,h,w].
 
     `frames` limits the batch (parity crops / CPU samples); `crop` takes the
     top-left (h, w) crop of every frame with its mask.
     """
     nb, h, w, patterns, _, _ = CONFIGS[cfg]
-    nb = nb if frames is None else frames
+    nb = nb - first if frames is None else frames
     hh, ww = (h, w) if crop is None else crop
     px = np.empty((nb, hh, ww), dtype=np.uint8)
     st = np.empty((nb, hh, ww), dtype=np.uint8)
-    for f in range(nb):
+    for i in range(nb):
+        f = first + i
         seed, noise, dens = frame_params(cfg, f)
-        px[f] = synth_frame(h, w, seed, noise, dens)[:hh, :ww]
-        st[f] = mask_for(patterns[f % len(patterns)], h, w, seed + 1)[:hh, :ww]
+        px[i] = synth_frame(h, w, seed, noise, dens)[:hh, :ww]
+        st[i] = mask_for(patterns[f % len(patterns)], h, w, seed + 1)[:hh, :ww]
     return px, st
