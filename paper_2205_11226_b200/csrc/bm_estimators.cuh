@@ -429,10 +429,16 @@ __device__ void hql_core(const Acc& acc, int m, EstSmem& S, double* __restrict__
       const double e = __shfl_sync(FULL, eps_lane, g);
       if (e < best_eps) { best_eps = e; best = g; }
     }
+    // near-tie gap of the beta choice (parity diagnostics), in units of the
+    // eps change a 1e-11 relative input perturbation can cause
+    double ya = lane < n ? fabs(S.y0[lane]) : 0.0;
+    ya = warp_max(ya);
+    const double dy = 1e-11 * ya;
+    const double noise = 2.0 * sqrt(best_eps * n) * dy + n * dy * dy + 1e-300;
     double gap = INFINITY;
     for (int g = 0; g < NBETA; g++) {
       const double e = __shfl_sync(FULL, eps_lane, g);
-      if (g != best) gap = fmin(gap, (e - best_eps) / (best_eps > 0.0 ? best_eps : 1.0));
+      if (g != best) gap = fmin(gap, fabs(e - best_eps) / noise);
     }
     if (lane == 0) {
       S.beta = ldexp(1.0, best - 8);

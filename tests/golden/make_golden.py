@@ -86,7 +86,9 @@ def run_case(name, pixels, states, profile, forced=None):
             w = ref.estimators._weights_from_quadforms(d, b)
             eps.append(float(((y0 - w @ y) ** 2).sum()))
         best = eps[int(np.where(ref.estimators.BETA_GRID == beta)[0][0])]
-        others = [(e - best) / (best if best > 0 else 1.0) for b, e in zip(ref.estimators.BETA_GRID, eps) if b != beta]
+        dy = 1e-11 * float(np.max(np.abs(y0)))
+        noise = 2.0 * np.sqrt(best * len(y0)) * dy + len(y0) * dy * dy + 1e-300
+        others = [abs(e - best) / noise for b, e in zip(ref.estimators.BETA_GRID, eps) if b != beta]
         gaps.append(min(others))
         return beta
 

@@ -7,8 +7,9 @@ divergence rule:
   * a mismatch is ALLOWED only when it is decided at a threshold or by
     rounding: |phi - T_phi| <= TOL*max(1,|T_phi|), |nu - T_nu| <= TOL*max(1,T_nu)
     on either side's score, or a beta grid choice whose reference epsilon gap
-    (bm_patch_record.beta_gap) is below BETA_TIE (the eps curve is flat to
-    rounding there);
+    (bm_patch_record.beta_gap: min |eps_g - eps_best| in units of the eps
+    change a 1e-11 relative input perturbation can cause) is below BETA_TIE,
+    i.e. the reference's beta choice is decided at rounding level;
   * after an allowed divergence the rest of that cell and all of its
     later-raster 8-neighbour descendants are excluded from pixel checks;
   * on the remaining lost pixels: |d| <= 1e-3 * max(|ref|, 1) and the u8
@@ -23,7 +24,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 TOL = 1e-5
-BETA_TIE = 1e-9
+BETA_TIE = 1.0
 REL = 1e-3
 
 

@@ -273,7 +273,7 @@ def test_hql_estimates_vs_oracle(native):
         assert g.layer.value == ["BRL", "IDL", "HQL"][info["layer"]]
         if g.layer is Layer.HQL:
             if g.diagnostics.bandwidth.beta != info["beta"]:
-                assert info["beta_gap"] < 1e-9  # rounding-decided grid near-tie
+                assert info["beta_gap"] < parity.BETA_TIE  # rounding-decided grid near-tie
                 continue
             assert abs(g.diagnostics.bandwidth.alpha - info["alpha"]) < 1e-7
         assert np.allclose(g.values, vals, rtol=1e-9, atol=1e-9)
