@@ -29,6 +29,7 @@
 #include "../../include/blockmend_b200.h"
 #include "bm_common.cuh"
 #include "bm_estimators.cuh"
+#include "bm_hql.cuh"
 
 namespace bm {
 
@@ -80,6 +81,8 @@ struct CellSmem {
   long long t_start;
   unsigned long long cnt[8];  // BRL IDL HQL deferred | flop64 flop32 hql gate
   EstSmem est;
+  HqlSmem hql;
+  HqlOut hout;
 };
 
 __device__ __forceinline__ int patch_r(int p) { return BS + 2 * (p >> 3); }  // tile coords of patch p
@@ -434,7 +437,7 @@ __device__ void write_record(const KParams& P, CellSmem& S, const bm_patch_recor
 }
 
 // One patch: gate + estimate (select_and_estimate / _forced_estimate).
-__device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV, double* gQ) {
+__device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS) {
   const int tid = threadIdx.x;
   EstSmem& E = S.est;
   const int pr_t = patch_r(p), pc_t = patch_c(p);
@@ -508,16 +511,21 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gV,
       // HQL with its ladder (estimators.py:248-286)
       bool done = false;
       if (m >= 2) {
-        hql_core(acc, m, E, gV, gQ);
-        if (E.ok) {
+        hql_columns(S.hql, E.n, E.uoff);
+        __syncthreads();
+        ZView zv{S.tile, S.cand};
+        hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout);
+        __syncthreads();
+        if (S.hout.ok) {
           done = true;
           if (tid == 0) {
+            for (int q = 0; q < 4; q++) E.vals[q] = S.hout.vals[q];
             S.cnt[4] += hql_flops(m, E.n);
             S.cnt[6]++;
             rec.layer = BM_LAYER_HQL;
-            rec.beta = E.beta;
-            rec.alpha = E.alpha;
-            rec.beta_gap = E.gap;
+            rec.beta = S.hout.beta;
+            rec.alpha = S.hout.alpha;
+            rec.beta_gap = S.hout.gap;
             rec.flags |= BM_REC_HAS_BW;
           }
         }
@@ -638,12 +646,11 @@ __device__ void pick_and_extract(CellSmem& S) {
   }
 }
 
-__global__ void __launch_bounds__(NT, 1) k_conceal(KParams P) {
+__global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CellSmem& S = *reinterpret_cast<CellSmem*>(smem_raw);
   const int tid = threadIdx.x;
-  double* gV = P.scratch + (size_t)blockIdx.x * P.scratch_per_cta;
-  double* gQ = gV + (size_t)MAXCAND * 32;
+  double* gS = P.scratch + (size_t)blockIdx.x * P.scratch_per_cta;
   if (tid < 8) S.cnt[tid] = 0;
   const int nslots = *((volatile int*)P.nslots);
   for (;;) {
@@ -707,7 +714,7 @@ __global__ void __launch_bounds__(NT, 1) k_conceal(KParams P) {
           __syncthreads();
           continue;
         }
-        estimate_patch(P, S, S.pick, gV, gQ);
+        estimate_patch(P, S, S.pick, gS);
         if (tid == 0) S.progressed = 1;
         __syncthreads();
       }
@@ -825,6 +832,8 @@ struct EstBatchArgs {
 
 struct EstBatchSmem {
   EstSmem est;
+  HqlSmem hql;
+  HqlOut hout;
 };
 
 __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
@@ -835,15 +844,21 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
   const int n = A.n_y[i], m = A.m[i];
   const double* X = A.x + (size_t)i * A.max_m * 4;
   const double* Y = A.y + (size_t)i * A.max_m * 32;
+  double* gs = A.scratch + (size_t)blockIdx.x * HQL_SCRATCH_DENSE;
   if (tid < 32) {
     E.y0[tid] = tid < n ? A.y0[(size_t)i * 32 + tid] : 0.0;
     E.y0f[tid] = (float)E.y0[tid];
   }
   if (tid == 0) E.n = n;
+  // dense Z [m][40]: y | x | 1 (the HQL column convention)
+  double* Z = gs + HQL_Z;
+  for (int o = tid; o < m * 40; o += NT) {
+    const int j = o / 40, c = o % 40;
+    Z[o] = c < n ? Y[(size_t)j * 32 + c] : (c >= 32 && c < 36 ? X[(size_t)j * 4 + c - 32] : (c == 36 ? 1.0 : 0.0));
+  }
+  hql_columns(S.hql, n, nullptr);
   __syncthreads();
   DenseAcc acc{X, Y};
-  double* gV = A.scratch + (size_t)blockIdx.x * ((size_t)MAXCAND * (32 + KMAX));
-  double* gQ = gV + (size_t)MAXCAND * 32;
   bm_patch_record rec;
   memset(&rec, 0, sizeof(rec));
   rec.nu = rec.beta = rec.alpha = __longlong_as_double(0x7ff8000000000000ll);
@@ -853,14 +868,18 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
   int layer = BM_LAYER_BRL, fallback = 0;
   bool done = false;
   if (A.layer == BM_LAYER_HQL && m >= 2) {
-    hql_core(acc, m, E, gV, gQ);
-    if (E.ok) {
+    ZView zv{Z, nullptr};
+    hql_mma(zv, m, n, E.y0, S.hql, gs, S.hout);
+    __syncthreads();
+    if (S.hout.ok) {
       done = true;
       layer = BM_LAYER_HQL;
-      rec.beta = E.beta;
-      rec.alpha = E.alpha;
-      rec.beta_gap = E.gap;
+      rec.beta = S.hout.beta;
+      rec.alpha = S.hout.alpha;
+      rec.beta_gap = S.hout.gap;
       rec.flags |= BM_REC_HAS_BW;
+      if (tid == 0)
+        for (int q = 0; q < 4; q++) E.vals[q] = S.hout.vals[q];
     }
   }
   if (!done && A.layer != BM_LAYER_BRL && m >= 1) {
@@ -927,6 +946,22 @@ int sm_count() {
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
+bool g_attr_set = false;
+
+// resident concealment CTAs per SM (persistent grid = SMs x this)
+int cells_per_sm() {
+  static int occ = 0;
+  if (!occ) {
+    const int smem = (int)sizeof(CellSmem);
+    if (!g_attr_set) {
+      if (cudaFuncSetAttribute(k_conceal, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess)
+        g_attr_set = true;
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_conceal, NT, smem) != cudaSuccess || occ < 1) occ = 1;
+  }
+  return occ;
+}
+
 bool params_ok(const bm_params* p) {
   return p && p->frames >= 1 && p->height >= 1 && p->width >= 1 && (p->pixel_dtype == BM_PIX_U8 || p->pixel_dtype == BM_PIX_F64) &&
          p->forced_layer >= -1 && p->forced_layer <= 2 && p->sigma2 > 0.0;
@@ -959,10 +994,11 @@ Layout layout(const bm_params* p) {
                                   (unsigned*)nullptr, (int)nc);
   L.cub_bytes = b1 > b2 ? b1 : b2;
   L.off_cub = o; o = align_up(o + L.cub_bytes);
-  const int sms = sm_count();
-  L.grid = (int)(nc < (size_t)sms ? nc : (size_t)sms);
+  const int per_sm = cells_per_sm();
+  const size_t cap = (size_t)sm_count() * per_sm;
+  L.grid = (int)(nc < cap ? nc : cap);
   if (L.grid < 1) L.grid = 1;
-  L.scratch_per_cta = (size_t)MAXCAND * (32 + KMAX);
+  L.scratch_per_cta = HQL_SCRATCH_FUSED;
   L.off_scratch = o; o = align_up(o + (size_t)L.grid * L.scratch_per_cta * 8);
   L.total = o;
   return L;
@@ -976,7 +1012,6 @@ int cuda_status(cudaError_t e) {
   return BM_OK;
 }
 
-bool g_attr_set = false;
 constexpr int NEV = 256;
 cudaEvent_t g_ev[NEV][2];
 bool g_ev_init = false;
@@ -1163,7 +1198,7 @@ int bm_estimate_batch(int32_t layer, int32_t count, int32_t max_m, double sigma2
   cudaStream_t stream = (cudaStream_t)stream_;
   cudaError_t e;
   double* scratch = nullptr;
-  const size_t per = (size_t)MAXCAND * (32 + KMAX);
+  const size_t per = HQL_SCRATCH_DENSE;
   if ((e = cudaMallocAsync((void**)&scratch, (size_t)count * per * 8, stream)) != cudaSuccess) return cuda_status(e);
   EstBatchArgs A{layer, count, max_m, sigma2, n_y, m, y0, x, y, out_values, out_info, scratch};
   const size_t smem = sizeof(EstBatchSmem);

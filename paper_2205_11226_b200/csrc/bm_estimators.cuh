@@ -48,28 +48,9 @@ struct EstSmem {
   float gap;
   int layer, fallback, ok;
   // reductions
-  double red[NWARP][40];
+  double red[NWARP][8];
   double redmin[NWARP];
-  int redidx[NWARP];
   float redf[NWARP];
-  // HQL
-  double mean[36];
-  double cyy[32 * 33];   // C_YY + ridge (row stride 33)
-  double cxy[4 * 32];
-  double L[32 * 33];     // Cholesky factor, padded to 32 with identity
-  double rdiag[32];
-  double P[NBETA][40];   // beta-grid weighted sums (y 0..31, S at 32, x at 33..36)
-  double xt[4], yt[32];  // x~0, y~0 at the chosen beta
-  int near[KMAX];
-  double vnear[KMAX][32];
-  double qmin[KMAX];
-  double xp[KMAX][4];
-  double yp[KMAX][32];
-  double cmat[4 * KMAX], rmat[4 * KMAX];
-  double dq[MAXCAND];    // Mahalanobis quadforms d_j
-  double e2[MAXCAND];    // Euclidean squared distances (alpha's nearest set)
-  uint8_t sel[MAXCAND];
-  double cpart[NT * 16]; // covariance block partials
 };
 
 // ----------------------------------------------------------------- helpers
@@ -98,30 +79,25 @@ __device__ __forceinline__ float cta_minf(float v, EstSmem& S) {
   return r;
 }
 
-// Sum 32 per-thread accumulators (+ up to 8 extra scalars) over the CTA;
-// result lands in out[0..31] and out[32..32+nx) (shared).  Fixed order.
-template <int NX>
-__device__ __forceinline__ void cta_sum40(double (&v)[32], double (&xs)[NX], double* out, EstSmem& S) {
+// CTA-wide sums of N per-thread values, fixed order; every thread gets the totals.
+template <int N>
+__device__ __forceinline__ void cta_sum_n(double (&v)[N], EstSmem& S) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double r = warp_reduce_scatter32(v, lane);
-  double xr[NX];
 #pragma unroll
-  for (int i = 0; i < NX; i++) xr[i] = warp_sum(xs[i]);
+  for (int i = 0; i < N; i++) v[i] = warp_sum(v[i]);
   __syncthreads();
-  S.red[w][lane] = r;
-  if (lane < NX) {
+  if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < NX; i++)
-      if (lane == i) S.red[w][32 + i] = xr[i];
+    for (int i = 0; i < N; i++) S.red[w][i] = v[i];
   }
   __syncthreads();
-  if (threadIdx.x < 32 + NX) {
-    double a = S.red[0][threadIdx.x];
 #pragma unroll
-    for (int i = 1; i < NWARP; i++) a += S.red[i][threadIdx.x];
-    out[threadIdx.x] = a;
+  for (int i = 0; i < N; i++) {
+    double a = S.red[0][i];
+#pragma unroll
+    for (int k = 1; k < NWARP; k++) a += S.red[k][i];
+    v[i] = a;
   }
-  __syncthreads();
 }
 
 // ----------------------------------------------------------------------- BRL
@@ -134,6 +110,7 @@ __device__ __forceinline__ void brl_values(EstSmem& S) {
   }
 }
 
+// ----------------------------------------------------------------------- IDL
 // Pairwise (NumPy) sum of v[i]^2 for i < n with v in registers.
 __device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
   if (n < 8) {
@@ -157,442 +134,55 @@ __device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
   return res;
 }
 
-// ----------------------------------------------------------------------- IDL
 // idl_weights / idl_estimate (estimators.py:112-132) in FP64, mirroring the
 // reference's arithmetic: d2 in NumPy's pairwise order, expo = -d2/(2 s2 N_y),
 // w = exp(expo - max) / sum, values = w @ x.  (The FP32 Nadaraya-Watson
 // distance/weight work is the nu gate's screening pass in gather(); FP32 in
 // the *estimate* itself is amplified ~1e4x along the patch chain and breaks
-// the +-1 LSB bar.)
+// the +-1 LSB bar.)  Per-candidate values stay in registers.
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
 template <class Acc>
 __device__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S) {
   const int n = S.n;
   const double c = 2.0 * sigma2 * n;
+  double ex[MAXCAND / NT];
   double emax = -INFINITY;
-  for (int j = threadIdx.x; j < m; j += NT) {
-    double v[32];
 #pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
-    const double expo = -pairwise_sq32(v, n) / c;
-    S.dq[j] = expo;
-    emax = fmax(emax, expo);
+  for (int i = 0; i < MAXCAND / NT; i++) {
+    const int j = threadIdx.x + i * NT;
+    ex[i] = -INFINITY;
+    if (j < m) {
+      double v[32];
+#pragma unroll
+      for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
+      ex[i] = -pairwise_sq32(v, n) / c;
+      emax = fmax(emax, ex[i]);
+    }
   }
   emax = -cta_min(-emax, S);
-  double xs[5] = {0, 0, 0, 0, 0};
-  double vz[32];
+  double tot[1] = {0.0};
 #pragma unroll
-  for (int t = 0; t < 32; t++) vz[t] = 0.0;
-  for (int j = threadIdx.x; j < m; j += NT) {
-    const double sh = exp(S.dq[j] - emax);
-    S.e2[j] = sh;
-    xs[0] += sh;
+  for (int i = 0; i < MAXCAND / NT; i++) {
+    ex[i] = (threadIdx.x + i * NT < m) ? exp(ex[i] - emax) : 0.0;  // shifted weights
+    tot[0] += ex[i];
   }
-  cta_sum40<1>(vz, *reinterpret_cast<double(*)[1]>(xs), S.P[0], S);
-  const double tot = S.P[0][32];
-  xs[0] = 0.0;
-  for (int j = threadIdx.x; j < m; j += NT) {
-    const double w = S.e2[j] / tot;
+  cta_sum_n<1>(tot, S);
+  double xs[4] = {0, 0, 0, 0};
 #pragma unroll
-    for (int q = 0; q < 4; q++) xs[1 + q] = fma(w, acc.x(j, q), xs[1 + q]);
+  for (int i = 0; i < MAXCAND / NT; i++) {
+    const int j = threadIdx.x + i * NT;
+    if (j < m) {
+      const double w = ex[i] / tot[0];
+#pragma unroll
+      for (int q = 0; q < 4; q++) xs[q] = fma(w, acc.x(j, q), xs[q]);
+    }
   }
-#pragma unroll
-  for (int t = 0; t < 32; t++) vz[t] = 0.0;
-  cta_sum40<5>(vz, xs, S.P[1], S);
+  cta_sum_n<4>(xs, S);
   if (threadIdx.x == 0) {
     const double e0 = exp(emax);  // raw_sum == 0.0 iff the largest term underflows
-    S.nu_raw = e0 * tot;
+    S.nu_raw = e0 * tot[0];
     S.ok = e0 != 0.0;
-    for (int q = 0; q < 4; q++) S.vals[q] = S.P[1][33 + q];
-  }
-  __syncthreads();
-}
-
-// ----------------------------------------------------------------------- HQL
-
-// Forward substitution L v = b (L padded to 32 with identity), in place.
-__device__ __forceinline__ void fwd_solve32(const double* L, const double* rdiag, double (&v)[32]) {
-#pragma unroll
-  for (int t = 0; t < 32; t++) {
-    double s = v[t];
-#pragma unroll
-    for (int k = 0; k < t; k++) s = fma(-L[t * 33 + k], v[k], s);
-    v[t] = s * rdiag[t];
-  }
-}
-// Back substitution L^T x = v, in place.
-__device__ __forceinline__ void bwd_solve32(const double* L, const double* rdiag, double (&v)[32]) {
-#pragma unroll
-  for (int t = 31; t >= 0; t--) {
-    double s = v[t];
-#pragma unroll
-    for (int k = t + 1; k < 32; k++) s = fma(-L[k * 33 + t], v[k], s);
-    v[t] = s * rdiag[t];
-  }
-}
-
-// Full HQL pipeline (estimators.py:256-273).  Returns via S: ok (0 -> the
-// IDL/BRL ladder must run), vals, beta, alpha, gap.  gV/gQ: per-CTA global
-// scratch of MAXCAND*32 and MAXCAND*KMAX doubles.
-template <class Acc>
-__device__ void hql_core(const Acc& acc, int m, EstSmem& S, double* __restrict__ gV, double* __restrict__ gQ) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int n = S.n, D = n + 4;
-
-  // ---- means over z = [y | x] (sample_covariance, estimators.py:140-141)
-  {
-    double* part = S.cpart;
-    if (tid < 252) {
-      const int k = tid % 36, s = tid / 36;
-      double a = 0.0;
-      if (k < D)
-        for (int j = s; j < m; j += 7) a += k < n ? acc.y(j, k) : acc.x(j, k - n);
-      part[s * 36 + k] = a;
-    }
-    __syncthreads();
-    if (tid < D) {
-      double a = 0.0;
-      for (int s = 0; s < 7; s++) a += part[s * 36 + tid];
-      S.mean[tid] = a / m;
-    }
-    __syncthreads();
-  }
-
-  // ---- covariance blocks C_YY (n x n) and C_XY (4 x n) (estimators.py:142-150)
-  {
-    const int nq = (n + 3) >> 2;          // y quads; x quad has index nq
-    const int nb = (nq + 1) * (nq + 2) / 2 - 1;
-    const int ns = min(8, NT / nb);
-    if (tid < nb * ns) {
-      const int blk = tid % nb, sl = tid / nb;
-      int qa = 0, qb = 0, c = blk;
-      for (qa = 0; qa <= nq; qa++) {
-        int len = nq - qa + 1;
-        if (qa == nq) len = 0;  // (x, x) skipped
-        if (c < len) { qb = qa + c; break; }
-        c -= len;
-      }
-      int da[4], db[4];
-      bool va[4], vb[4];
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        da[e] = qa < nq ? 4 * qa + e : n + e;
-        va[e] = qa < nq ? (4 * qa + e < n) : true;
-        db[e] = qb < nq ? 4 * qb + e : n + e;
-        vb[e] = qb < nq ? (4 * qb + e < n) : true;
-      }
-      double ma[4], mb[4];
-#pragma unroll
-      for (int e = 0; e < 4; e++) {
-        ma[e] = va[e] ? S.mean[da[e]] : 0.0;
-        mb[e] = vb[e] ? S.mean[db[e]] : 0.0;
-      }
-      double a16[16];
-#pragma unroll
-      for (int e = 0; e < 16; e++) a16[e] = 0.0;
-      for (int j = sl; j < m; j += ns) {
-        double za[4], zb[4];
-#pragma unroll
-        for (int e = 0; e < 4; e++) {
-          za[e] = va[e] ? (da[e] < n ? acc.y(j, da[e]) : acc.x(j, da[e] - n)) - ma[e] : 0.0;
-          zb[e] = vb[e] ? (db[e] < n ? acc.y(j, db[e]) : acc.x(j, db[e] - n)) - mb[e] : 0.0;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; e++)
-#pragma unroll
-          for (int f = 0; f < 4; f++) a16[e * 4 + f] = fma(za[e], zb[f], a16[e * 4 + f]);
-      }
-#pragma unroll
-      for (int e = 0; e < 16; e++) S.cpart[(sl * nb + blk) * 16 + e] = a16[e];
-    }
-    __syncthreads();
-    for (int o = tid; o < nb * 16; o += NT) {
-      const int blk = o / 16, e = (o % 16) / 4, f = o % 4;
-      double a = 0.0;
-      for (int s = 0; s < ns; s++) a += S.cpart[(s * nb + blk) * 16 + e * 4 + f];
-      a = a / (double)(m - 1);
-      int qa = 0, qb = 0, c = blk;
-      for (qa = 0; qa <= nq; qa++) {
-        int len = nq - qa + 1;
-        if (qa == nq) len = 0;
-        if (c < len) { qb = qa + c; break; }
-        c -= len;
-      }
-      const int ia = qa < nq ? 4 * qa + e : n + e;
-      const int ib = qb < nq ? 4 * qb + f : n + f;
-      const bool oka = qa < nq ? ia < n : true, okb = qb < nq ? ib < n : true;
-      if (oka && okb) {
-        if (ia < n && ib < n) {
-          S.cyy[ia * 33 + ib] = a;
-          S.cyy[ib * 33 + ia] = a;
-        } else if (ia < n && ib >= n) {
-          S.cxy[(ib - n) * 32 + ia] = a;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      const double tr = pairwise_sum_n(n, [&](int i) { return S.cyy[i * 33 + i]; });
-      const double ridge = tr > 0.0 ? 1e-6 * tr / n : 1e-6;  // estimators.py:148-150
-      for (int i = 0; i < n; i++) S.cyy[i * 33 + i] += ridge;
-    }
-    __syncthreads();
-  }
-
-  // ---- Cholesky (CovarianceBlocks._factor, estimators.py:61-64), warp 0
-  if (warp == 0) {
-    bool fail = false;
-    for (int j = 0; j < 32; j++) {
-      if (j < n) {
-        double t = 0.0;
-        if (lane >= j && lane < n) {
-          t = S.cyy[lane * 33 + j];
-          for (int k = 0; k < j; k++) t = fma(-S.L[lane * 33 + k], S.L[j * 33 + k], t);
-        }
-        const double s = __shfl_sync(FULL, t, j);
-        if (!(s > 0.0)) { fail = true; break; }
-        const double d = sqrt(s);
-        if (lane == j) S.L[j * 33 + j] = d;
-        if (lane > j && lane < n) S.L[lane * 33 + j] = t / d;
-        if (lane < j) S.L[lane * 33 + j] = 0.0;
-      } else {
-        S.L[lane * 33 + j] = lane == j ? 1.0 : (lane > j ? 0.0 : (lane < n ? 0.0 : 0.0));
-      }
-      __syncwarp();
-    }
-    // rows >= n: identity padding
-    if (!fail && lane >= n)
-      for (int k = 0; k < 32; k++) S.L[lane * 33 + k] = (k == lane) ? 1.0 : 0.0;
-    __syncwarp();
-    if (!fail) S.rdiag[lane] = 1.0 / S.L[lane * 33 + lane];
-    if (lane == 0) S.ok = !fail;
-  }
-  __syncthreads();
-  if (!S.ok) return;
-
-  // ---- quadforms d_j = ||L^-1 (y0 - y_j)||^2 (_context_quadforms 154-158)
-  //      and Euclidean e2_j (optimize_alpha 222), v_j -> gV
-  double dloc = INFINITY;
-  for (int j = tid; j < m; j += NT) {
-    double v[32];
-#pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = t < n ? S.y0[t] - acc.y(j, t) : 0.0;
-    S.e2[j] = pairwise_sq32(v, n);
-    fwd_solve32(S.L, S.rdiag, v);
-    double d = 0.0;
-#pragma unroll
-    for (int t = 0; t < 32; t++) {
-      d = fma(v[t], v[t], d);
-      gV[(size_t)t * MAXCAND + j] = v[t];
-    }
-    S.dq[j] = d;
-    dloc = fmin(dloc, d);
-  }
-  const double dmin = cta_min(dloc, S);
-
-  // ---- beta grid search (_beta_search 197-206)
-  for (int g = 0; g < NBETA; g++) {
-    const double s = ldexp(1.0, 7 - g);  // 1 / (2 beta), beta = 2^(g-8)
-    double v[32];
-    double xs[1] = {0.0};
-#pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = 0.0;
-    for (int j = tid; j < m; j += NT) {
-      const double w = exp((dmin - S.dq[j]) * s);  // exp(expo - expo.max()), exact scaling by 2^k
-      xs[0] += w;
-#pragma unroll
-      for (int t = 0; t < 32; t++)
-        if (t < n) v[t] = fma(w, acc.y(j, t), v[t]);
-    }
-    cta_sum40<1>(v, xs, S.P[g], S);
-  }
-  if (warp == 0) {
-    // eps_g = ||y0 - (w @ y)||^2, strict < argmin (ties -> smaller beta)
-    double eps_lane = 0.0;  // lane g holds eps_g
-    for (int g = 0; g < NBETA; g++) {
-      double e = 0.0;
-      if (lane < n) {
-        const double yt = S.P[g][lane] / S.P[g][32];
-        const double d = S.y0[lane] - yt;
-        e = __dmul_rn(d, d);
-      }
-      // pairwise order over n (NumPy .sum())
-      S.red[0][lane] = e;
-      __syncwarp();
-      double eps = pairwise_sum_n(n, [&](int i) { return S.red[0][i]; });
-      __syncwarp();
-      if (lane == g) eps_lane = eps;
-    }
-    double best_eps = INFINITY;
-    int best = 0;
-    for (int g = 0; g < NBETA; g++) {
-      const double e = __shfl_sync(FULL, eps_lane, g);
-      if (e < best_eps) { best_eps = e; best = g; }
-    }
-    // near-tie gap of the beta choice (parity diagnostics), in units of the
-    // eps change a 1e-11 relative input perturbation can cause
-    double ya = lane < n ? fabs(S.y0[lane]) : 0.0;
-    ya = warp_max(ya);
-    const double dy = 1e-11 * ya;
-    const double noise = 2.0 * sqrt(best_eps * n) * dy + n * dy * dy + 1e-300;
-    double gap = INFINITY;
-    for (int g = 0; g < NBETA; g++) {
-      const double e = __shfl_sync(FULL, eps_lane, g);
-      if (g != best) gap = fmin(gap, fabs(e - best_eps) / noise);
-    }
-    if (lane == 0) {
-      S.beta = ldexp(1.0, best - 8);
-      S.gap = (float)gap;
-      S.near[0] = best;  // temp: grid index
-    }
-  }
-  __syncthreads();
-  const int gbest = S.near[0];
-  const double sb = ldexp(1.0, 7 - gbest);
-  __syncthreads();
-
-  // ---- x~0, y~0 at beta (estimators.py:262-264)
-  {
-    double v[32];
-    double xs[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = 0.0;
-    for (int j = tid; j < m; j += NT) {
-      const double w = exp((dmin - S.dq[j]) * sb);
-      xs[0] += w;
-#pragma unroll
-      for (int q = 0; q < 4; q++) xs[1 + q] = fma(w, acc.x(j, q), xs[1 + q]);
-#pragma unroll
-      for (int t = 0; t < 32; t++)
-        if (t < n) v[t] = fma(w, acc.y(j, t), v[t]);
-    }
-    cta_sum40<5>(v, xs, S.P[0], S);
-    if (tid < 32) S.yt[tid] = S.P[0][tid] / S.P[0][32];
-    if (tid < 4) S.xt[tid] = S.P[0][33 + tid] / S.P[0][32];
-    __syncthreads();
-  }
-
-  // ---- alpha (optimize_alpha, estimators.py:209-245); m >= 2 here
-  const int k = min(n + 1, m);
-  for (int j = tid; j < m; j += NT) S.sel[j] = 0;
-  __syncthreads();
-  for (int i = 0; i < k; i++) {
-    // stable argsort of e2: smallest (e2, index) not yet taken
-    double bv = INFINITY;
-    int bj = 0x7fffffff;
-    for (int j = tid; j < m; j += NT) {
-      if (S.sel[j]) continue;
-      const double e = S.e2[j];
-      if (e < bv || (e == bv && j < bj)) { bv = e; bj = j; }
-    }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(FULL, bv, o);
-      const int oj = __shfl_xor_sync(FULL, bj, o);
-      if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
-    }
-    if (lane == 0) { S.redmin[warp] = bv; S.redidx[warp] = bj; }
-    __syncthreads();
-    if (tid == 0) {
-      double v = S.redmin[0];
-      int jj = S.redidx[0];
-      for (int w = 1; w < NWARP; w++)
-        if (S.redmin[w] < v || (S.redmin[w] == v && S.redidx[w] < jj)) { v = S.redmin[w]; jj = S.redidx[w]; }
-      S.near[i] = jj;
-      S.sel[jj] = 1;
-    }
-    __syncthreads();
-  }
-  for (int o = tid; o < k * 32; o += NT) S.vnear[o / 32][o % 32] = gV[(size_t)(o % 32) * MAXCAND + S.near[o / 32]];
-  __syncthreads();
-  // q_ij = (y_i - y_j)^T C^-1 (y_i - y_j) = ||v_i - v_j||^2  (estimators.py:225-229)
-  for (int j = tid; j < m; j += NT) {
-    double v[32];
-#pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = gV[(size_t)t * MAXCAND + j];
-    for (int i = 0; i < k; i++) {
-      double q = 0.0;
-#pragma unroll
-      for (int t = 0; t < 32; t++) {
-        const double d = S.vnear[i][t] - v[t];
-        q = fma(d, d, q);
-      }
-      gQ[(size_t)i * MAXCAND + j] = q;
-    }
-  }
-  __syncthreads();
-  // row minima over j != nearest_i (expo.max with the LOO -inf, 231-233)
-  for (int i = 0; i < k; i++) {
-    double mn = INFINITY;
-    const int ni = S.near[i];
-    for (int j = tid; j < m; j += NT)
-      if (j != ni) mn = fmin(mn, gQ[(size_t)i * MAXCAND + j]);
-    mn = cta_min(mn, S);
-    if (tid == 0) S.qmin[i] = mn;
-  }
-  __syncthreads();
-  // LOO predictions x_i~, y_i~ (estimators.py:231-238)
-  for (int i = 0; i < k; i++) {
-    const int ni = S.near[i];
-    const double qm = S.qmin[i];
-    double v[32];
-    double xs[5] = {0, 0, 0, 0, 0};
-#pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = 0.0;
-    for (int j = tid; j < m; j += NT) {
-      if (j == ni) continue;
-      const double w = exp((qm - gQ[(size_t)i * MAXCAND + j]) * sb);
-      xs[0] += w;
-#pragma unroll
-      for (int q = 0; q < 4; q++) xs[1 + q] = fma(w, acc.x(j, q), xs[1 + q]);
-#pragma unroll
-      for (int t = 0; t < 32; t++)
-        if (t < n) v[t] = fma(w, acc.y(j, t), v[t]);
-    }
-    cta_sum40<5>(v, xs, S.P[1], S);
-    if (tid < 32) S.yp[i][tid] = S.P[1][tid] / S.P[1][32];
-    if (tid < 4) S.xp[i][tid] = S.P[1][33 + tid] / S.P[1][32];
-    __syncthreads();
-  }
-  // correction directions c_i = C_XY C^-1 (y_i - y~_i), residuals x_i - x~_i (239-244)
-  if (tid < k) {
-    const int i = tid, ni = S.near[i];
-    double v[32];
-#pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(ni, t) - S.yp[i][t] : 0.0;
-    fwd_solve32(S.L, S.rdiag, v);
-    bwd_solve32(S.L, S.rdiag, v);
-    for (int q = 0; q < 4; q++) {
-      double c = 0.0;
-      for (int a = 0; a < n; a++) c = fma(S.cxy[q * 32 + a], v[a], c);
-      S.cmat[q * k + i] = c;
-      S.rmat[q * k + i] = acc.x(ni, q) - S.xp[i][q];
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    const int kk = 4 * k;
-    const double den = pairwise_sum_n(kk, [&](int i) { return __dmul_rn(S.cmat[i], S.cmat[i]); });
-    const double num = pairwise_sum_n(kk, [&](int i) { return __dmul_rn(S.rmat[i], S.cmat[i]); });
-    double a = 0.0;
-    if (!(den < 1e-12)) {
-      a = num / den;
-      a = a < 0.0 ? 0.0 : (a > 4.0 ? 4.0 : a);  // np.clip (NaN propagates)
-    }
-    S.alpha = a;
-    // values = x~0 + alpha * C_XY C^-1 (y0 - y~0)   (estimators.py:266)
-    double v[32];
-    for (int t = 0; t < 32; t++) v[t] = t < n ? S.y0[t] - S.yt[t] : 0.0;
-    fwd_solve32(S.L, S.rdiag, v);
-    bwd_solve32(S.L, S.rdiag, v);
-    bool finite = true;
-    for (int q = 0; q < 4; q++) {
-      double c = 0.0;
-      for (int t = 0; t < n; t++) c = fma(S.cxy[q * 32 + t], v[t], c);
-      S.vals[q] = S.xt[q] + a * c;
-      if (!isfinite(S.vals[q])) finite = false;
-    }
-    S.ok = finite;  // FloatingPointError -> ladder (estimators.py:267-268)
+    for (int q = 0; q < 4; q++) S.vals[q] = xs[q];
   }
   __syncthreads();
 }

@@ -73,9 +73,15 @@ def compare(ref_out, ref_recs, test_out, test_recs, states, t_phi, t_nu) -> Pari
         res.ok = False
         res.problems.append(f"cell sets differ: {sorted(set(rc) ^ set(tc))[:5]}")
         return res
-    diverged = set()
-    for cell, ri in rc.items():
-        ti = tc[cell]
+    # cells in (frame, raster) order; a cell with a diverged / excluded
+    # earlier-raster 8-neighbour legitimately reads different values
+    excl = set()
+    for cell in sorted(rc):
+        f, cr, cc = cell
+        if any((f, cr + dr, cc + dc) in excl for dr, dc in ((-1, -1), (-1, 0), (-1, 1), (0, -1))):
+            excl.add(cell)
+            continue
+        ri, ti = rc[cell], tc[cell]
         for k in range(max(len(ri), len(ti))):
             if k >= len(ri) or k >= len(ti):
                 res.ok = False
@@ -109,20 +115,8 @@ def compare(ref_out, ref_recs, test_out, test_recs, states, t_phi, t_nu) -> Pari
                     f"phi={b['phi']} nu={b['nu']}")
             else:
                 res.allowed.append(f"{where}: {excuse}")
-            diverged.add(cell)
+            excl.add(cell)
             break
-    # exclude diverged cells and their later-raster 8-neighbour descendants
-    lost_cells = set(rc)
-    order = sorted(lost_cells)
-    excl = set(diverged)
-    for cell in order:
-        if cell in excl:
-            continue
-        f, r, c = cell
-        for dr, dc in ((-1, -1), (-1, 0), (-1, 1), (0, -1)):
-            if (f, r + dr, c + dc) in excl:
-                excl.add(cell)
-                break
     res.excluded_cells = excl
     lost = states == 1
     keep = lost.copy()
