@@ -38,11 +38,14 @@ class ParityResult:
     u8_off: int = 0
     max_rel: float = 0.0
     max_u8: int = 0
+    u8_off_all: int = 0  # over ALL lost pixels, excluded cells included
+    lost_pixels: int = 0
 
     def summary(self) -> str:
         return (f"ok={self.ok} problems={len(self.problems)} allowed={len(self.allowed)} "
                 f"excluded_cells={len(self.excluded_cells)} checked_px={self.checked_pixels} "
-                f"u8_off={self.u8_off} max_u8={self.max_u8} max_rel={self.max_rel:.2e}")
+                f"u8_off={self.u8_off} max_u8={self.max_u8} max_rel={self.max_rel:.2e} "
+                f"u8_off_all={self.u8_off_all}/{self.lost_pixels}")
 
 
 def _cells_of(recs):
@@ -119,6 +122,10 @@ def compare(ref_out, ref_recs, test_out, test_recs, states, t_phi, t_nu) -> Pari
             break
     res.excluded_cells = excl
     lost = states == 1
+    res.lost_pixels = int(lost.sum())
+    qa_all = np.floor(np.clip(ref_out[lost], 0, 255) + 0.5)
+    qb_all = np.floor(np.clip(test_out[lost], 0, 255) + 0.5)
+    res.u8_off_all = int((qa_all != qb_all).sum())
     keep = lost.copy()
     for f, r, c in excl:
         keep[f, r * 16 : (r + 1) * 16, c * 16 : (c + 1) * 16] = False
