@@ -8,6 +8,7 @@ CUDA device is present, every compute call raises NativeUnavailableError.
 from __future__ import annotations
 
 import ctypes
+import glob
 import os
 import subprocess
 
@@ -16,7 +17,7 @@ from .errors import DimensionMismatchError, NativeUnavailableError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
 SOURCES = [os.path.join(PKG_DIR, "csrc", "bm_conceal.cu")]
-HEADERS = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_common.cuh", "bm_estimators.cuh")] + [
+HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh"))) + [
     os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
 ]
 NVCC_FLAGS = [
@@ -62,7 +63,7 @@ class Summary(ctypes.Structure):
 SUMMARY_BYTES = ctypes.sizeof(Summary)
 EXPORTS = [
     "bm_abi_version", "bm_status_string", "bm_workspace_bytes", "bm_max_records", "bm_device_clock_khz",
-    "bm_kernel_times_ms", "bm_kernel_times_reset",
+    "bm_kernel_times_ms", "bm_kernel_times_reset", "bm_debug_phase_cycles",
     "bm_conceal", "bm_compact_records", "bm_conceal_host", "bm_estimate_batch",
 ]
 
@@ -113,6 +114,8 @@ def lib():
     L.bm_kernel_times_ms.restype = ctypes.c_int
     L.bm_kernel_times_ms.argtypes = [ctypes.POINTER(ctypes.c_float), ctypes.c_int]
     L.bm_kernel_times_reset.restype = None
+    L.bm_debug_phase_cycles.restype = ctypes.c_int
+    L.bm_debug_phase_cycles.argtypes = [ctypes.POINTER(ctypes.c_uint64), ctypes.c_int]
     L.bm_conceal.restype = ctypes.c_int
     L.bm_conceal.argtypes = [ctypes.POINTER(Params), vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]
     L.bm_compact_records.restype = ctypes.c_int
@@ -156,3 +159,13 @@ def kernel_times_ms() -> list[float]:
 
 def kernel_times_reset() -> None:
     lib().bm_kernel_times_reset()
+
+
+PHASES = ["gate", "means", "covariance", "cholesky", "linv", "quadforms", "dmin", "beta", "nearest", "staging",
+          "gram", "loo", "alpha", "patch_brl", "patch_idl", "patch_hql"]
+
+
+def phase_cycles(reset: bool = True) -> dict:
+    buf = (ctypes.c_uint64 * 16)()
+    check(lib().bm_debug_phase_cycles(buf, int(reset)))
+    return {name: int(buf[i]) for i, name in enumerate(PHASES)}

@@ -65,9 +65,9 @@ struct CellSmem {
   uint64_t lostbits[TILE];
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
-  float rbuf[NT];
-  int pref[NT];
-  int wcnt[NWARP];
+  float rbuf[2 * NT];
+  int pref[2 * NT];
+  int wcnt[2 * NWARP];
   int ring_off[MAXRING + 2];
   // per-patch control (written by warp 0 / thread 0, read after a barrier)
   int ticket, slot, f, gr, gc;
@@ -321,51 +321,70 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     return;
   }
   const float invf = (float)(1.0 / (2.0 * P.sigma2 * n));
-  for (int e0 = 0; e0 < K; e0 += NT) {
-    const int e = e0 + tid;
-    bool adm = false;
-    float rw = 0.f;
-    int pos = 0;
-    if (e < K) {
-      int r = 1;
-      while (r < max_ring && S.ring_off[r + 1] <= e) r++;
-      int a, b;
-      ring_entry(g, r, e - S.ring_off[r], a, b);
-      const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
-      adm = true;
+  constexpr int GH = 2, GCH = GH * NT;  // entries per chunk: GH per thread
+  for (int e0 = 0; e0 < K; e0 += GCH) {
+    bool adm[GH];
+    int pos[GH];
 #pragma unroll
-      for (int q = 0; q < 6; q++)
-        if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) adm = false;
-      if (adm) {
-        pos = wr * TS + wc;
-        if (gated) {
-          // nu screening: FP32 Nadaraya-Watson distance + weight
-          // (raw_idl_weights, estimators.py:105-109)
-          const float* tp = S.tile32 + pos;
-          float d2 = 0.f;
-          for (int k = 0; k < n; k++) {
-            const float d = tp[E.uoff[k]] - E.y0f[k];
-            d2 = fmaf(d, d, d2);
+    for (int h = 0; h < GH; h++) {
+      const int e = e0 + h * NT + tid;
+      adm[h] = false;
+      pos[h] = 0;
+      float rw = 0.f;
+      if (e < K) {
+        int r = 1;
+        while (r < max_ring && S.ring_off[r + 1] <= e) r++;
+        int a, b;
+        ring_entry(g, r, e - S.ring_off[r], a, b);
+        const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
+        bool ok = true;
+#pragma unroll
+        for (int q = 0; q < 6; q++)
+          if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) ok = false;
+        adm[h] = ok;
+        if (ok) {
+          pos[h] = wr * TS + wc;
+          if (gated) {
+            // nu screening: FP32 Nadaraya-Watson distance + weight
+            // (raw_idl_weights, estimators.py:105-109)
+            const float* tp = S.tile32 + pos[h];
+            float d2a = 0.f, d2b = 0.f;
+            int k = 0;
+            for (; k + 2 <= n; k += 2) {
+              const float da = tp[E.uoff[k]] - E.y0f[k];
+              const float db = tp[E.uoff[k + 1]] - E.y0f[k + 1];
+              d2a = fmaf(da, da, d2a);
+              d2b = fmaf(db, db, d2b);
+            }
+            if (k < n) {
+              const float da = tp[E.uoff[k]] - E.y0f[k];
+              d2a = fmaf(da, da, d2a);
+            }
+            rw = expf(-(d2a + d2b) * invf);
           }
-          rw = expf(-d2 * invf);
         }
       }
+      const unsigned bal = __ballot_sync(FULL, adm[h]);
+      if (lane == 0) S.wcnt[h * NWARP + warp] = __popc(bal);
+      S.rbuf[h * NT + tid] = adm[h] ? rw : 0.f;
     }
-    // ordered compaction
-    const unsigned bal = __ballot_sync(FULL, adm);
-    const int wpre = __popc(bal & ((1u << lane) - 1));
-    if (lane == 0) S.wcnt[warp] = __popc(bal);
-    S.rbuf[tid] = adm ? rw : 0.f;
     __syncthreads();
-    int base = 0, tot = 0;
-#pragma unroll
-    for (int w = 0; w < NWARP; w++) {
-      if (w < warp) base += S.wcnt[w];
-      tot += S.wcnt[w];
-    }
+    // ordered compaction (entries are in (h, warp, lane) = expansion-map order)
     const int m0 = S.m_total;
-    if (adm) S.cand[m0 + base + wpre] = (uint16_t)pos;
-    S.pref[tid] = base + wpre + (adm ? 1 : 0);  // inclusive count up to e
+    int tot = 0;
+#pragma unroll
+    for (int h = 0; h < GH; h++) {
+      int base = tot;
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) {
+        if (w < warp) base += S.wcnt[h * NWARP + w];
+        tot += S.wcnt[h * NWARP + w];
+      }
+      const unsigned bal = __ballot_sync(FULL, adm[h]);
+      const int wpre = __popc(bal & ((1u << lane) - 1));
+      if (adm[h]) S.cand[m0 + base + wpre] = (uint16_t)pos[h];
+      S.pref[h * NT + tid] = base + wpre + (adm[h] ? 1 : 0);  // inclusive count up to e
+    }
     __syncthreads();
     if (!gated) {
       if (tid == 0) S.m_total = m0 + tot;
@@ -374,7 +393,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     }
     // nu bookkeeping, ring by ring (warp 0)
     if (warp == 0) {
-      const int e1 = min(e0 + NT, K);
+      const int e1 = min(e0 + GCH, K);
       int r = S.cur_ring + 1;
       double carry = S.carry, nu = S.nu;
       int stop = 0;
@@ -511,6 +530,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
       // HQL with its ladder (estimators.py:248-286)
       bool done = false;
       if (m >= 2) {
+        if (tid == 0) atomicAdd(&g_phase_cycles[0], (unsigned long long)(clock64() - S.t_start));
         hql_columns(S.hql, E.n, E.uoff);
         __syncthreads();
         ZView zv{S.tile, S.cand};
@@ -579,6 +599,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
   }
   if (tid == 0) {
     rec.cycles = (uint32_t)(clock64() - S.t_start);
+    atomicAdd(&g_phase_cycles[13 + (rec.layer == BM_LAYER_HQL ? 2 : rec.layer)], (unsigned long long)rec.cycles);
     write_record(P, S, rec);
     S.nrec++;
     S.cnt[rec.layer]++;
@@ -1022,6 +1043,15 @@ int g_nev = 0;
 extern "C" {
 
 int bm_abi_version(void) { return BM_ABI_VERSION; }
+
+int bm_debug_phase_cycles(unsigned long long* out16, int reset) {
+  if (cudaMemcpyFromSymbol(out16, g_phase_cycles, 16 * 8) != cudaSuccess) return BM_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[16] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, 16 * 8);
+  }
+  return BM_OK;
+}
 
 int bm_kernel_times_ms(float* out, int cap) {
   int n = g_nev < cap ? g_nev : cap;

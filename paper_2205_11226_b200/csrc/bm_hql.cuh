@@ -36,6 +36,12 @@ struct ZView {
 
 constexpr int LS = 36;  // stride of Linv / Vn: conflict-free A-fragment loads (36 = 4 mod 16)
 
+constexpr int RED_HALF = NWARP / 2;
+constexpr int ZP_OFF = RED_HALF * 20 * 32;          // Zp rows after the 20-tile partials
+constexpr int R1_SIZE = (RED_HALF * 30 * 32 > ZP_OFF + KMAX * 40 ? RED_HALF * 30 * 32 : ZP_OFF + KMAX * 40) > 2 * 32 * 33
+                            ? (RED_HALF * 30 * 32 > ZP_OFF + KMAX * 40 ? RED_HALF * 30 * 32 : ZP_OFF + KMAX * 40)
+                            : 2 * 32 * 33;
+
 struct HqlSmem {
   int16_t coff[40];
   double cconst[40];
@@ -43,10 +49,10 @@ struct HqlSmem {
   double Linv[32 * LS];
   double Bm[4 * 32];     // C_XY L^-T
   double cxy[4 * 32];
-  double R1[3840];       // tree-reduction partials / cyy+L / u
-  double R2[1600];       // P (24x40) / Vn (40x36) / Zp (40x40)
+  double R1[R1_SIZE];    // tree-reduction partials / cyy+L / [ZP_OFF..): Zp rows < 33 / u
+  double R2[1600];       // P (24x40) / Vn (40x36)
   double wmin[NWARP][40];
-  double qmin[40];
+  double rdiag[32];
   double dn[40];
   int near[40];
   double cmat[4 * KMAX], rmat[4 * KMAX];
@@ -59,8 +65,7 @@ struct HqlSmem {
 
 // per-CTA global scratch (doubles)
 constexpr size_t HQL_V = 0;                                  // V   [32][MAXCAND]
-constexpr size_t HQL_Q = HQL_V + (size_t)32 * MAXCAND;       // q   [MAXCAND/8][5][32][2] fragment-native
-constexpr size_t HQL_D = HQL_Q + (size_t)(MAXCAND / 8) * 5 * 64;
+constexpr size_t HQL_D = HQL_V + (size_t)32 * MAXCAND;
 constexpr size_t HQL_E2 = HQL_D + MAXCAND;
 constexpr size_t HQL_Z = HQL_E2 + MAXCAND;                   // dense Z [MAXCAND][40] (estimator API only)
 constexpr size_t HQL_SCRATCH_FUSED = HQL_Z;
@@ -70,39 +75,23 @@ __device__ __forceinline__ double zval(const double* ptr, int b, int off, double
   return off >= 0 ? ptr[b + off] : cst;
 }
 
-// Fixed-order tree reduction of per-warp register tiles (8 warps -> warp 0).
+// Fixed-order tree reduction of per-warp register tiles (NWARP warps -> warp 0);
+// red must hold (NWARP/2) * N * 32 doubles.
 template <int N>
 __device__ __forceinline__ void tree_reduce(double (&acc)[N], double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __syncthreads();
-  if (warp >= 4) {
 #pragma unroll
-    for (int i = 0; i < N; i++) red[((warp - 4) * N + i) * 32 + lane] = acc[i];
-  }
-  __syncthreads();
-  if (warp < 4) {
+  for (int half = NWARP / 2; half >= 1; half >>= 1) {
+    __syncthreads();
+    if (warp >= half && warp < 2 * half) {
 #pragma unroll
-    for (int i = 0; i < N; i++) acc[i] += red[(warp * N + i) * 32 + lane];
-  }
-  __syncthreads();
-  if (warp == 2 || warp == 3) {
+      for (int i = 0; i < N; i++) red[((warp - half) * N + i) * 32 + lane] = acc[i];
+    }
+    __syncthreads();
+    if (warp < half) {
 #pragma unroll
-    for (int i = 0; i < N; i++) red[((warp - 2) * N + i) * 32 + lane] = acc[i];
-  }
-  __syncthreads();
-  if (warp < 2) {
-#pragma unroll
-    for (int i = 0; i < N; i++) acc[i] += red[(warp * N + i) * 32 + lane];
-  }
-  __syncthreads();
-  if (warp == 1) {
-#pragma unroll
-    for (int i = 0; i < N; i++) red[i * 32 + lane] = acc[i];
-  }
-  __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int i = 0; i < N; i++) acc[i] += red[i * 32 + lane];
+      for (int i = 0; i < N; i++) acc[i] += red[(warp * N + i) * 32 + lane];
+    }
   }
 }
 
@@ -125,6 +114,18 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
 
 // The HQL pipeline for one patch.  Inputs: zv (candidates), m >= 2, n, y0
 // (shared, [32]).  Outputs in H/out: ok, vals[4], beta, alpha, gap.
+// Per-phase cycle accounting of the HQL pipeline (thread 0, after barriers);
+// read back with bm_debug_phase_cycles.  Phase 0 = everything before HQL.
+__device__ unsigned long long g_phase_cycles[16];
+#define BM_PHASE(k)                                                    \
+  do {                                                                 \
+    if (threadIdx.x == 0) {                                            \
+      const long long now_ = clock64();                                \
+      atomicAdd(&g_phase_cycles[k], (unsigned long long)(now_ - ph_t)); \
+      ph_t = now_;                                                     \
+    }                                                                  \
+  } while (0)
+
 struct HqlOut {
   double vals[4];
   double beta, alpha;
@@ -137,9 +138,8 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   double* gV = gs + HQL_V;
-  double* gQ = gs + HQL_Q;
   double* gD = gs + HQL_D;
-  double* gE2 = gs + HQL_E2;
+  long long ph_t = clock64();
   const int nks = (m + 3) >> 2;  // k-steps of 4 candidates
   const int nct = (m + 7) >> 3;  // column tiles of 8 candidates
 
@@ -163,6 +163,7 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       H.mean[tid] = s / m;  // z.mean(axis=0)
     }
     __syncthreads();
+    BM_PHASE(1);
   }
 
   // ------------------------------------------------- covariance (DMMA)
@@ -179,13 +180,19 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     double acc[28];
 #pragma unroll
     for (int i = 0; i < 28; i++) acc[i] = 0.0;
-    for (int s = warp; s < nks; s += NWARP) {
+    // software pipeline: the next k-step's fragments load during this step's MMAs
+    double f[5], fn[5];
+    auto load_f = [&](int s, double(&o)[5]) {
       const int j = 4 * s + t4;
-      const bool valid = j < m;
+      const bool valid = s < nks && j < m;
       const int b = valid ? zv.base(j) : 0;
-      double f[5];
 #pragma unroll
-      for (int tl = 0; tl < 5; tl++) f[tl] = valid ? zval(zv.ptr, b, off[tl], cst[tl]) - mu[tl] : 0.0;
+      for (int tl = 0; tl < 5; tl++) o[tl] = valid ? zval(zv.ptr, b, off[tl], cst[tl]) - mu[tl] : 0.0;
+    };
+    load_f(warp, f);
+#pragma unroll 1
+    for (int s = warp; s < nks; s += NWARP) {
+      load_f(s + NWARP, fn);
       int idx = 0;
 #pragma unroll
       for (int a = 0; a < 4; a++)
@@ -194,10 +201,13 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
           dmma(acc[2 * idx], acc[2 * idx + 1], f[a], f[bb]);
           idx++;
         }
+#pragma unroll
+      for (int tl = 0; tl < 5; tl++) f[tl] = fn[tl];
     }
     tree_reduce<28>(acc, H.R1);
-    double* cyy = H.R1 + 3840 - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
+    double* cyy = H.R1 + R1_SIZE - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
     double* L = cyy + 32 * 33;
+    __syncwarp();
     if (warp == 0) {
       const double inv = 1.0 / (double)(m - 1);
       int idx = 0;
@@ -223,11 +233,13 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       (void)inv;
     }
     __syncthreads();
-    // ridge (estimators.py:148-150) and Cholesky (CovarianceBlocks._factor)
+    BM_PHASE(2);
+    // ridge (estimators.py:148-150) and Cholesky (CovarianceBlocks._factor) on
+    // warp 0; meanwhile warps 1..7 compute the Euclidean distances in NumPy's
+    // order (optimize_alpha's nearest set, estimators.py:222)
     if (warp == 0) {
-      double tr = 0.0;
       if (lane == 0) {
-        tr = pairwise_sum_n(n, [&](int i) { return cyy[i * 33 + i]; });
+        const double tr = pairwise_sum_n(n, [&](int i) { return cyy[i * 33 + i]; });
         const double ridge = tr > 0.0 ? 1e-6 * tr / n : 1e-6;
         for (int i = 0; i < n; i++) cyy[i * 33 + i] += ridge;
       }
@@ -236,43 +248,110 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       for (int j = 0; j < n; j++) {
         double t = 0.0;
         if (lane >= j && lane < n) {
-          t = cyy[lane * 33 + j];
-          for (int k = 0; k < j; k++) t = fma(-L[lane * 33 + k], L[j * 33 + k], t);
+          const double* Li = L + lane * 33;
+          const double* Lj = L + j * 33;
+          double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+          int k = 0;
+          for (; k + 4 <= j; k += 4) {
+            t0 = fma(Li[k], Lj[k], t0);
+            t1 = fma(Li[k + 1], Lj[k + 1], t1);
+            t2 = fma(Li[k + 2], Lj[k + 2], t2);
+            t3 = fma(Li[k + 3], Lj[k + 3], t3);
+          }
+          for (; k < j; k++) t0 = fma(Li[k], Lj[k], t0);
+          t = cyy[lane * 33 + j] - ((t0 + t1) + (t2 + t3));
         }
         const double sd = __shfl_sync(FULL, t, j);
         if (!(sd > 0.0)) { fail = true; break; }
-        const double d = sqrt(sd);
-        if (lane == j) L[j * 33 + j] = d;
-        if (lane > j && lane < n) L[lane * 33 + j] = t / d;
+        const double rs = rsqrt(sd);  // 1 / L_jj
+        if (lane == j) {
+          L[j * 33 + j] = sd * rs;
+          H.rdiag[j] = rs;
+        }
+        if (lane > j && lane < n) L[lane * 33 + j] = t * rs;
         __syncwarp();
       }
       if (lane == 0) H.fail = fail;
-      __syncwarp();
-      if (!fail) {
-        // L^-1, one column per lane (forward substitution on e_c), identity beyond n
-        const int c = lane;
-        for (int i = 0; i < 32; i++) {
-          double x;
-          if (i < c) x = 0.0;
-          else if (i >= n) x = (i == c) ? 1.0 : 0.0;
-          else if (i == c) x = 1.0 / L[i * 33 + i];
-          else {
-            double s = 0.0;
-            for (int k = c; k < i; k++) s = fma(L[i * 33 + k], H.Linv[k * LS + c], s);
-            x = -s / L[i * 33 + i];
-          }
-          H.Linv[i * LS + c] = x;
+    } else {
+      // warps 1..7: Euclidean distances in NumPy's order and the stable
+      // k-nearest selection (optimize_alpha, estimators.py:221-223)
+      constexpr int NW7 = NT - 32, PER = (MAXCAND + NW7 - 1) / NW7;
+      const int t7 = tid - 32, w7 = warp - 1;
+      double ev[PER];
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        const int j = t7 + i * NW7;
+        ev[i] = INFINITY;
+        if (j < m) {
+          const int b = zv.base(j);
+          double v[32];
+#pragma unroll
+          for (int t = 0; t < 32; t++) v[t] = t < n ? zv.ptr[b + H.coff[t]] - y0[t] : 0.0;
+          ev[i] = pairwise_sq32(v, n);
         }
+      }
+      const int k = min(n + 1, m);
+      unsigned taken = 0;
+      for (int it = 0; it < k; it++) {
+        double bv = INFINITY;
+        int bj = 0x7fffffff;
+#pragma unroll
+        for (int i = 0; i < PER; i++) {
+          const int j = t7 + i * NW7;
+          if (!((taken >> i) & 1u) && (ev[i] < bv || (ev[i] == bv && j < bj))) { bv = ev[i]; bj = j; }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const double ov = __shfl_xor_sync(FULL, bv, o);
+          const int oj = __shfl_xor_sync(FULL, bj, o);
+          if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+        }
+        const int slot = it & 1;
+        if (lane == 0) { H.redmin[slot][w7] = bv; H.redidx[slot][w7] = bj; }
+        asm volatile("bar.sync 1, %0;" ::"r"(NW7) : "memory");  // warps 1..NWARP-1
+        double v = H.redmin[slot][0];
+        int jj = H.redidx[slot][0];
+#pragma unroll
+        for (int w = 1; w < NWARP - 1; w++)
+          if (H.redmin[slot][w] < v || (H.redmin[slot][w] == v && H.redidx[slot][w] < jj)) {
+            v = H.redmin[slot][w];
+            jj = H.redidx[slot][w];
+          }
+        if ((jj % NW7) == t7) taken |= 1u << (jj / NW7);
+        if (t7 == 0) H.near[it] = jj;
       }
     }
     __syncthreads();
+    BM_PHASE(3);
     if (H.fail) {
       if (tid == 0) out.ok = 0;
       return;
     }
+    // L^-1 (forward substitution on e_c), identity beyond n: warp w owns
+    // columns w, w+NWARP, ...; LPC = NWARP lanes split each dot product
+    {
+      constexpr int LPC = NWARP;
+      const int c = warp + NWARP * (lane / LPC), sub = lane % LPC;
+      for (int i = 0; i < 32; i++) {
+        double s = 0.0;
+        if (i < n && i > c)
+          for (int k = c + sub; k < i; k += LPC) s = fma(L[i * 33 + k], H.Linv[k * LS + c], s);
+#pragma unroll
+        for (int o = 1; o < LPC; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
+        double x;
+        if (i < c) x = 0.0;
+        else if (i >= n) x = (i == c) ? 1.0 : 0.0;
+        else if (i == c) x = H.rdiag[i];
+        else x = -s * H.rdiag[i];
+        if (sub == 0) H.Linv[i * LS + c] = x;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    BM_PHASE(4);
     // Bm = C_XY L^-T : Bm[q][t] = sum_s C_XY[q][s] Linv[t][s]
-    if (tid < 128) {
-      const int q = tid >> 5, t = tid & 31;
+    for (int o = tid; o < 128; o += NT) {
+      const int q = o >> 5, t = o & 31;
       double s = 0.0;
       for (int k = 0; k < n; k++) s = fma(H.cxy[q * 32 + k], H.Linv[t * LS + k], s);
       H.Bm[q * 32 + t] = t < n ? s : 0.0;
@@ -289,24 +368,35 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       y0r[kk] = dim < n ? y0[dim] : 0.0;
       offy[kk] = H.coff[dim];
     }
-    for (int c = warp; c < nct; c += NWARP) {
+    double fb[8], fbn[8];
+    auto load_v = [&](int c, double(&o)[8]) {
       const int jB = 8 * c + g;
-      const bool vb = jB < m;
+      const bool vb = c < nct && jB < m;
       const int bB = vb ? zv.base(jB) : 0;
-      double fb[8];
 #pragma unroll
       for (int kk = 0; kk < 8; kk++) {
         const int dim = 4 * kk + t4;
-        fb[kk] = (vb && dim < n) ? y0r[kk] - zv.ptr[bB + offy[kk]] : 0.0;
+        o[kk] = (vb && dim < n) ? y0r[kk] - zv.ptr[bB + offy[kk]] : 0.0;
       }
-      double acc[8];
+    };
+    load_v(warp, fb);
+#pragma unroll 1
+    for (int c = warp; c < nct; c += NWARP) {
+      load_v(c + NWARP, fbn);
+      double acc[8], acb[8];  // even / odd k-steps: two independent MMA chains
 #pragma unroll
-      for (int i = 0; i < 8; i++) acc[i] = 0.0;
+      for (int i = 0; i < 8; i++) acc[i] = acb[i] = 0.0;
 #pragma unroll
       for (int r = 0; r < 4; r++)
 #pragma unroll
-        for (int kk = 0; kk < 2 * r + 2; kk++)
-          dmma(acc[2 * r], acc[2 * r + 1], H.Linv[(8 * r + g) * LS + 4 * kk + t4], fb[kk]);
+        for (int kk = 0; kk < 2 * r + 2; kk++) {
+          if (kk & 1) dmma(acb[2 * r], acb[2 * r + 1], H.Linv[(8 * r + g) * LS + 4 * kk + t4], fb[kk]);
+          else dmma(acc[2 * r], acc[2 * r + 1], H.Linv[(8 * r + g) * LS + 4 * kk + t4], fb[kk]);
+        }
+#pragma unroll
+      for (int i = 0; i < 8; i++) acc[i] += acb[i];
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) fb[kk] = fbn[kk];
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int r = 0; r < 4; r++) {
@@ -328,16 +418,9 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
         if (col + 1 < m) gD[col + 1] = s1;
       }
     }
-    // Euclidean distances in NumPy's order (optimize_alpha's nearest set, estimators.py:222)
-    for (int j = tid; j < m; j += NT) {
-      const int b = zv.base(j);
-      double v[32];
-#pragma unroll
-      for (int t = 0; t < 32; t++) v[t] = t < n ? zv.ptr[b + H.coff[t]] - y0[t] : 0.0;
-      gE2[j] = pairwise_sq32(v, n);
-    }
   }
   __syncthreads();
+  BM_PHASE(5);
   double dmin;
   {
     double mn = INFINITY;
@@ -345,6 +428,7 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     mn = warp_min(mn);
     if (lane == 0) H.redmin[0][warp] = mn;
     __syncthreads();
+    BM_PHASE(6);
     dmin = H.redmin[0][0];
 #pragma unroll
     for (int w = 1; w < NWARP; w++) dmin = fmin(dmin, H.redmin[0][w]);
@@ -359,29 +443,40 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     cstz[ct] = H.cconst[8 * ct + g];
   }
   {
-    double sc[3];
-#pragma unroll
-    for (int r = 0; r < 3; r++) sc[r] = ldexp(1.0, 7 - (8 * r + g));  // 1/(2 beta)
+    // MMA row 8r+g holds grid point beta_(3g+r): a lane's three betas are
+    // consecutive, so one exp at beta_(3g+2) and two squarings give all three
+    // (w(2^-1 beta) = w(beta)^2 exactly in real arithmetic; <= 4 ulp here)
+    const double sc2 = ldexp(1.0, 7 - (3 * g + 2));  // 1/(2 beta_(3g+2))
+    const bool brow = 3 * g + 2 < NBETA;
     double acc[30];
 #pragma unroll
     for (int i = 0; i < 30; i++) acc[i] = 0.0;
-    for (int s = warp; s < nks; s += NWARP) {
+    // software pipeline: next k-step's d_j and B fragments load during this step
+    double dl, dln, fb[5], fbn[5];
+    auto load_b = [&](int s, double& d, double(&o)[5]) {
       const int j = 4 * s + t4;
-      const bool valid = j < m;
+      const bool valid = s < nks && j < m;
       const int b = valid ? zv.base(j) : 0;
-      const double delta = valid ? dmin - gD[j] : 0.0;
-      double fa[3], fb[5];
+      d = valid ? dmin - gD[j] : -INFINITY;  // -inf -> weight 0 for padding
 #pragma unroll
-      for (int r = 0; r < 3; r++) {
-        const int gi = 8 * r + g;
-        fa[r] = (valid && gi < NBETA) ? exp(delta * sc[r]) : 0.0;  // exp(expo - expo.max())
-      }
-#pragma unroll
-      for (int ct = 0; ct < 5; ct++) fb[ct] = valid ? zval(zv.ptr, b, offz[ct], cstz[ct]) : 0.0;
+      for (int ct = 0; ct < 5; ct++) o[ct] = valid ? zval(zv.ptr, b, offz[ct], cstz[ct]) : 0.0;
+    };
+    load_b(warp, dl, fb);
+#pragma unroll 1
+    for (int s = warp; s < nks; s += NWARP) {
+      load_b(s + NWARP, dln, fbn);
+      double fa[3];
+      const double e2w = brow ? exp(dl * sc2) : 0.0;  // exp(expo - expo.max())
+      fa[2] = e2w;
+      fa[1] = e2w * e2w;
+      fa[0] = fa[1] * fa[1];
 #pragma unroll
       for (int r = 0; r < 3; r++)
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) dmma(acc[2 * (r * 5 + ct)], acc[2 * (r * 5 + ct) + 1], fa[r], fb[ct]);
+      dl = dln;
+#pragma unroll
+      for (int ct = 0; ct < 5; ct++) fb[ct] = fbn[ct];
     }
     tree_reduce<30>(acc, H.R1);
     double* P = H.R2;  // [24][40]
@@ -390,8 +485,11 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       for (int r = 0; r < 3; r++)
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
-          P[(8 * r + g) * 40 + 8 * ct + 2 * t4] = acc[2 * (r * 5 + ct)];
-          P[(8 * r + g) * 40 + 8 * ct + 2 * t4 + 1] = acc[2 * (r * 5 + ct) + 1];
+          const int bi = 3 * g + r;  // grid index of MMA row 8r+g
+          if (bi < 24) {
+            P[bi * 40 + 8 * ct + 2 * t4] = acc[2 * (r * 5 + ct)];
+            P[bi * 40 + 8 * ct + 2 * t4 + 1] = acc[2 * (r * 5 + ct) + 1];
+          }
         }
       __syncwarp();
       // eps_g = ||y0 - y~0(beta_g)||^2 in NumPy's pairwise order; strict < argmin
@@ -428,49 +526,11 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       }
     }
     __syncthreads();
+    BM_PHASE(7);
   }
   const double sb = ldexp(1.0, 7 - H.gbest);
   const int k = min(n + 1, m);
 
-  // ------------------------------- nearest k by Euclidean distance (stable)
-  {
-    double ev[MAXCAND / NT];
-#pragma unroll
-    for (int i = 0; i < MAXCAND / NT; i++) {
-      const int j = tid + i * NT;
-      ev[i] = j < m ? gE2[j] : INFINITY;
-    }
-    unsigned taken = 0;
-    for (int it = 0; it < k; it++) {
-      double bv = INFINITY;
-      int bj = 0x7fffffff;
-#pragma unroll
-      for (int i = 0; i < MAXCAND / NT; i++) {
-        const int j = tid + i * NT;
-        if (!((taken >> i) & 1u) && (ev[i] < bv || (ev[i] == bv && j < bj))) { bv = ev[i]; bj = j; }
-      }
-#pragma unroll
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(FULL, bv, o);
-        const int oj = __shfl_xor_sync(FULL, bj, o);
-        if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
-      }
-      const int slot = it & 1;
-      if (lane == 0) { H.redmin[slot][warp] = bv; H.redidx[slot][warp] = bj; }
-      __syncthreads();
-      double v = H.redmin[slot][0];
-      int jj = H.redidx[slot][0];
-#pragma unroll
-      for (int w = 1; w < NWARP; w++)
-        if (H.redmin[slot][w] < v || (H.redmin[slot][w] == v && H.redidx[slot][w] < jj)) {
-          v = H.redmin[slot][w];
-          jj = H.redidx[slot][w];
-        }
-      if ((jj % NT) == tid) taken |= 1u << (jj / NT);
-      if (tid == 0) H.near[it] = jj;
-    }
-    __syncthreads();
-  }
   // stage V columns of the nearest set: Vn[i][t] (A fragments of the Gram GEMM)
   double* Vn = H.R2;  // [40][LS]
   for (int o = tid; o < 40 * 32; o += NT) {
@@ -479,119 +539,134 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
   }
   if (tid < 40) H.dn[tid] = tid < k ? gD[H.near[tid]] : 0.0;
   __syncthreads();
+  BM_PHASE(9);
 
-  // ------------------- q_ij = (y_i - y_j)^T C^-1 (y_i - y_j) (DMMA Gram)
-  {
-    double mins[5];
-    int nr[5];
+  // ---- fused Gram + leave-one-out sums (estimators.py:225-238), DMMA.
+  // q_ij = d_i + d_j - 2 v_i.v_j (= (y_i-y_j)^T C^-1 (y_i-y_j)); the LOO
+  // weights exp(x_ij - max_j x_ij), x = -q/(2 beta), are accumulated with a
+  // lazily raised per-row reference max (rescale only when a new x exceeds it
+  // by > 20, so w <= e^20): identical to the reference's shift after the final
+  // normalisation, and q never round-trips through memory.  One 8-row tile
+  // per pass bounds registers (the V fragments are re-read from L2).
+  double* Zp = H.R1 + ZP_OFF;  // [KMAX][40], after the <=20-tile tree-reduction partials
+  const int npass = (k + 7) >> 3;  // one 8-row tile of the nearest set per pass
+  for (int pass = 0; pass < npass; pass++) {
+    constexpr int RR = 1;  // 8-row tiles per pass
+    const int r0 = pass, nrow = 1;
+    double xref[RR];
+    int nr[RR];
+    double dni[RR];
 #pragma unroll
-    for (int r = 0; r < 5; r++) {
-      mins[r] = INFINITY;
-      const int i = 8 * r + g;
-      nr[r] = i < k ? H.near[i] : -1;
-    }
-    for (int c = warp; c < nct; c += NWARP) {
-      const int jB = 8 * c + g;
-      double fb[8];
-#pragma unroll
-      for (int kk = 0; kk < 8; kk++) fb[kk] = jB < m ? gV[(size_t)(4 * kk + t4) * MAXCAND + jB] : 0.0;
-      const int col = 8 * c + 2 * t4;
-      const double d0 = col < m ? gD[col] : 0.0, d1 = col + 1 < m ? gD[col + 1] : 0.0;
-#pragma unroll
-      for (int r = 0; r < 5; r++) {
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 8; kk++) dmma(a0, a1, Vn[(8 * r + g) * LS + 4 * kk + t4], fb[kk]);
-        const int i = 8 * r + g;
-        const double di = H.dn[i];
-        const double q0 = di + d0 - 2.0 * a0, q1 = di + d1 - 2.0 * a1;
-        double* qp = gQ + ((size_t)(c * 5 + r) * 32 + lane) * 2;
-        qp[0] = q0;
-        qp[1] = q1;
-        if (i < k) {
-          if (col < m && col != nr[r]) mins[r] = fmin(mins[r], q0);
-          if (col + 1 < m && col + 1 != nr[r]) mins[r] = fmin(mins[r], q1);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 5; r++) {
-      mins[r] = fmin(mins[r], __shfl_xor_sync(FULL, mins[r], 1));
-      mins[r] = fmin(mins[r], __shfl_xor_sync(FULL, mins[r], 2));
-      if (t4 == 0) H.wmin[warp][8 * r + g] = mins[r];
-    }
-    __syncthreads();
-    if (tid < 40) {
-      double mn = H.wmin[0][tid];
-#pragma unroll
-      for (int w = 1; w < NWARP; w++) mn = fmin(mn, H.wmin[w][tid]);
-      H.qmin[tid] = mn;
-    }
-    __syncthreads();
-  }
-
-  // ------------------------ leave-one-out sums Zp = W [Y|X|1] (DMMA)
-  double* Zp = H.R2;  // [40][40] (Vn is dead)
-  for (int pass = 0; pass < 2; pass++) {
-    const int r0 = pass ? 3 : 0, nrow = pass ? 2 : 3;
-    double qm[3];
-    int nr[3];
-#pragma unroll
-    for (int rr = 0; rr < 3; rr++) {
+    for (int rr = 0; rr < RR; rr++) {
       const int i = 8 * (r0 + rr) + g;
-      qm[rr] = (rr < nrow && i < k) ? H.qmin[i] : 0.0;
-      nr[rr] = (rr < nrow && i < k) ? H.near[i] : -2;
+      const bool ok = rr < nrow && i < k;
+      nr[rr] = ok ? H.near[i] : -2;
+      dni[rr] = ok ? H.dn[i] : 0.0;
+      xref[rr] = -INFINITY;
     }
-    double acc[30];
+    double acc[10 * RR];
 #pragma unroll
-    for (int i = 0; i < 30; i++) acc[i] = 0.0;
+    for (int i = 0; i < 10 * RR; i++) acc[i] = 0.0;
     const int src0 = (g << 2) | (t4 >> 1), src1 = (g << 2) | (2 + (t4 >> 1));
+    double fv[8], fvn[8], dv[2], dvn[2];
+    auto load_g = [&](int c, double(&o)[8], double(&dd)[2]) {
+      const int jB = 8 * c + g;
+      const bool ok = c < nct && jB < m;
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) o[kk] = ok ? gV[(size_t)(4 * kk + t4) * MAXCAND + jB] : 0.0;
+      const int col = 8 * c + 2 * t4;
+      dd[0] = (c < nct && col < m) ? gD[col] : 0.0;
+      dd[1] = (c < nct && col + 1 < m) ? gD[col + 1] : 0.0;
+    };
+    load_g(warp, fv, dv);
+#pragma unroll 1
     for (int c = warp; c < nct; c += NWARP) {
-      double fb[2][5];
+      load_g(c + NWARP, fvn, dvn);
+      const int col = 8 * c + 2 * t4;
+      const double d0 = dv[0], d1 = dv[1];
+      double fz[2][5];
 #pragma unroll
       for (int ks = 0; ks < 2; ks++) {
         const int j = 8 * c + 4 * ks + t4;
         const bool valid = j < m;
         const int b = valid ? zv.base(j) : 0;
 #pragma unroll
-        for (int ct = 0; ct < 5; ct++) fb[ks][ct] = valid ? zval(zv.ptr, b, offz[ct], cstz[ct]) : 0.0;
+        for (int ct = 0; ct < 5; ct++) fz[ks][ct] = valid ? zval(zv.ptr, b, offz[ct], cstz[ct]) : 0.0;
       }
-      const int col = 8 * c + 2 * t4;
 #pragma unroll
-      for (int rr = 0; rr < 3; rr++) {
+      for (int rr = 0; rr < RR; rr++) {
         if (rr >= nrow) break;
-        const double* qp = gQ + ((size_t)(c * 5 + r0 + rr) * 32 + lane) * 2;
-        const double q0 = qp[0], q1 = qp[1];
-        double w0 = 0.0, w1 = 0.0;
-        if (nr[rr] >= 0) {
-          if (col < m && col != nr[rr]) w0 = exp((qm[rr] - q0) * sb);
-          if (col + 1 < m && col + 1 != nr[rr]) w1 = exp((qm[rr] - q1) * sb);
+        const int r = r0 + rr;
+        double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;  // two independent MMA chains
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += 2) {
+          dmma(g0, g1, Vn[(8 * r + g) * LS + 4 * kk + t4], fv[kk]);
+          dmma(h0, h1, Vn[(8 * r + g) * LS + 4 * kk + 4 + t4], fv[kk + 1]);
         }
+        g0 += h0;
+        g1 += h1;
+        double x0 = -INFINITY, x1 = -INFINITY;
+        if (nr[rr] >= 0) {
+          if (col < m && col != nr[rr]) x0 = -(dni[rr] + d0 - 2.0 * g0) * sb;
+          if (col + 1 < m && col + 1 != nr[rr]) x1 = -(dni[rr] + d1 - 2.0 * g1) * sb;
+        }
+        double tmax = fmax(x0, x1);
+        tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 1));
+        tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 2));
+        if (tmax > xref[rr] + 20.0) {  // raise the row's reference, rescale its partial sums
+          const double f = xref[rr] == -INFINITY ? 0.0 : exp(xref[rr] - tmax);
+#pragma unroll
+          for (int i = 0; i < 10; i++) acc[rr * 10 + i] *= f;
+          xref[rr] = tmax;
+        }
+        const double a0x = x0 - xref[rr], a1x = x1 - xref[rr];
+        const double w0 = a0x > -746.0 ? exp(a0x) : 0.0;  // exp underflows to 0 below
+        const double w1 = a1x > -746.0 ? exp(a1x) : 0.0;
         // C-fragment layout (row g, cols 2t4..2t4+1) -> A fragments of the two k-steps
-        const double x0 = __shfl_sync(FULL, w0, src0), x1 = __shfl_sync(FULL, w1, src0);
-        const double z0 = __shfl_sync(FULL, w0, src1), z1 = __shfl_sync(FULL, w1, src1);
-        const double a0 = (t4 & 1) ? x1 : x0, a1 = (t4 & 1) ? z1 : z0;
+        const double s0 = __shfl_sync(FULL, w0, src0), s1 = __shfl_sync(FULL, w1, src0);
+        const double u0 = __shfl_sync(FULL, w0, src1), u1 = __shfl_sync(FULL, w1, src1);
+        const double a0 = (t4 & 1) ? s1 : s0, a1 = (t4 & 1) ? u1 : u0;
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
-          dmma(acc[2 * (rr * 5 + ct)], acc[2 * (rr * 5 + ct) + 1], a0, fb[0][ct]);
-          dmma(acc[2 * (rr * 5 + ct)], acc[2 * (rr * 5 + ct) + 1], a1, fb[1][ct]);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, fz[0][ct]);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a1, fz[1][ct]);
         }
       }
+#pragma unroll
+      for (int kk = 0; kk < 8; kk++) fv[kk] = fvn[kk];
+      dv[0] = dvn[0];
+      dv[1] = dvn[1];
     }
-    tree_reduce<30>(acc, H.R1);
+    // combine the warps' partial sums at a common per-row reference
+#pragma unroll
+    for (int rr = 0; rr < RR; rr++)
+      if (t4 == 0) H.wmin[warp][rr * 8 + g] = xref[rr];
+    __syncthreads();
+#pragma unroll
+    for (int rr = 0; rr < RR; rr++) {
+      double mx = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) mx = fmax(mx, H.wmin[w][rr * 8 + g]);
+      const double f = (xref[rr] == -INFINITY) ? 0.0 : exp(xref[rr] - mx);
+#pragma unroll
+      for (int i = 0; i < 10; i++) acc[rr * 10 + i] *= f;
+    }
+    tree_reduce<10 * RR>(acc, H.R1);
     if (warp == 0) {
 #pragma unroll
-      for (int rr = 0; rr < 3; rr++) {
-        if (rr >= nrow) break;
+      for (int rr = 0; rr < RR; rr++) {
+        const int row = 8 * (r0 + rr) + g;
+        if (rr >= nrow || row >= KMAX) break;
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
-          Zp[(8 * (r0 + rr) + g) * 40 + 8 * ct + 2 * t4] = acc[2 * (rr * 5 + ct)];
-          Zp[(8 * (r0 + rr) + g) * 40 + 8 * ct + 2 * t4 + 1] = acc[2 * (rr * 5 + ct) + 1];
+          Zp[row * 40 + 8 * ct + 2 * t4] = acc[rr * 10 + 2 * ct];
+          Zp[row * 40 + 8 * ct + 2 * t4 + 1] = acc[rr * 10 + 2 * ct + 1];
         }
       }
     }
   }
   __syncthreads();
+  BM_PHASE(11);
 
   // ---------------------------------- alpha (estimators.py:237-245)
   {
@@ -608,8 +683,8 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       u[i * 32 + t] = t < n ? s : 0.0;
     }
     __syncthreads();
-    if (tid < 4 * k) {
-      const int q = tid / k, i = tid % k;
+    for (int o = tid; o < 4 * k; o += NT) {
+      const int q = o / k, i = o % k;
       double c = 0.0;
       for (int t = 0; t < n; t++) c = fma(H.Bm[q * 32 + t], u[i * 32 + t], c);
       const int b = zv.base(H.near[i]);
@@ -646,6 +721,7 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     }
   }
   __syncthreads();
+  BM_PHASE(12);
 }
 
 }  // namespace bm

@@ -1,0 +1,24 @@
+"""Dev tool: HQL phase cycle breakdown on a workload subset."""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2205_11226_b200 as bm
+from paper_2205_11226_b200 import _native
+from paper_2205_11226_b200.profiles import conceal_batch
+from paper_2205_11226_b200.synth import make_config
+cfg = int(sys.argv[1]); nf = int(sys.argv[2]); prof = sys.argv[3]
+px, st = make_config(cfg, frames=nf)
+p = bm.Profile.sentinel() if prof == 'sentinel' else bm.Profile.named(prof)
+tp, ts = torch.from_numpy(px).cuda(), torch.from_numpy(st).cuda()
+conceal_batch(tp, ts, p)
+_native.phase_cycles(reset=True)
+r = conceal_batch(tp, ts, p, time_kernel=True)
+ph = _native.phase_cycles(reset=True)
+n_hql = r.summary['hql_patches']
+tot = sum(v for k, v in ph.items() if not k.startswith('patch'))
+print('kernel ms', _native.kernel_times_ms()[-1], 'hql patches', n_hql, r.summary['layer_counts'])
+for k, v in ph.items():
+    if k.startswith('patch'):
+        print(f"{k:12s} total {v:.3e} cycles")
+    else:
+        print(f"{k:12s} {v / max(n_hql,1):10.0f} cycles/HQL patch  {100 * v / tot:5.1f}%")
