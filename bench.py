@@ -134,33 +134,40 @@ def _oracle_crop(args):
     return cells, time.perf_counter() - t0
 
 
-def cpu_baseline(workload: str, budget_s: float = 20.0, crop: int = 128):
-    """Oracle (plain-C port of the reference path) on the host cores over a
-    bounded sample: one crop x crop tile per worker, workers = host cores."""
-    from multiprocessing import Pool
-
-    from oracle import oracle
-
-    oracle.lib()  # build once before forking
+def cpu_jobs(workload: str, crop: int = 384):
+    """Bounded CPU sample of the workload: one crop x crop tile (multiple of 16)
+    per host core, from the workload's own frames; built outside any timing."""
     cfg, prof_name, forced = WORKLOADS[workload]
     prof = profile_of(prof_name)
     forced_code = -1 if forced is None else {"BRL": 0, "IDL": 1, "HQL": 2}[forced]
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     nb = CONFIGS[cfg][0]
-    jobs = []
     px_all, st_all = make_inputs(cfg, 0, min(nb, cores))
+    h, w = px_all.shape[1:]
+    crop = min(crop, h // 16 * 16, w // 16 * 16)
+    gy, gx = max(h // crop, 1), max(w // crop, 1)
+    jobs = []
     for i in range(cores):
         f = i % px_all.shape[0]
-        h, w = px_all.shape[1:]
-        # crops from a grid of positions inside the frame (multiples of 16)
-        gy = (h // crop)
-        gx = (w // crop)
         k = i // px_all.shape[0]
-        y0 = (k % max(gy, 1)) * crop
-        x0 = ((k // max(gy, 1)) % max(gx, 1)) * crop
-        c_px = px_all[f, y0 : y0 + crop, x0 : x0 + crop]
-        c_st = st_all[f, y0 : y0 + crop, x0 : x0 + crop]
-        jobs.append((c_px, c_st, prof.t_phi, prof.t_nu, forced_code))
+        y0 = (k % gy) * crop
+        x0 = ((k // gy) % gx) * crop
+        jobs.append((px_all[f, y0 : y0 + crop, x0 : x0 + crop], st_all[f, y0 : y0 + crop, x0 : x0 + crop],
+                     prof.t_phi, prof.t_nu, forced_code))
+    return jobs, cores, crop
+
+
+def cpu_baseline(workload: str, jobs=None):
+    """Oracle (plain-C FP64 port of the reference path) on all host cores over
+    the bounded sample of cpu_jobs (one process per core)."""
+    from multiprocessing import Pool
+
+    from oracle import oracle
+
+    oracle.lib()  # build once before forking
+    if jobs is None:
+        jobs = cpu_jobs(workload)
+    jobs, cores, crop = jobs
     t0 = time.perf_counter()
     with Pool(cores) as pool:
         res = pool.map(_oracle_crop, jobs)
@@ -171,7 +178,7 @@ def cpu_baseline(workload: str, budget_s: float = 20.0, crop: int = 128):
         "unit": UNIT,
         "cores": cores,
         "kind": "port",
-        "sample": f"{cores} crops {crop}x{crop} of {workload} frames ({cells} lost cells), one per core, "
+        "sample": f"{cores} crops {crop}x{crop} of {workload} frames ({cells} lost cells), one process per core, "
                   f"plain-C FP64 oracle, {wall:.1f}s wall",
     }
 
@@ -179,11 +186,12 @@ def cpu_baseline(workload: str, budget_s: float = 20.0, crop: int = 128):
 def run_reference(args, rank, world):
     if rank != 0:
         return
+    jobs = cpu_jobs(args.workload)
     times = []
     last = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        last = cpu_baseline(args.workload)
+        last = cpu_baseline(args.workload, jobs)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
     value = last["value"]
