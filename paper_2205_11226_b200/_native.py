@@ -162,7 +162,7 @@ def kernel_times_reset() -> None:
 
 
 PHASES = ["gate", "means", "covariance", "cholesky", "linv", "quadforms", "dmin", "beta", "nearest", "staging",
-          "gram", "loo", "alpha", "patch_brl", "patch_idl", "patch_hql"]
+          "gram", "loo", "alpha", "chol_only", "patch_idl", "patch_hql"]
 
 
 def phase_cycles(reset: bool = True) -> dict:

@@ -599,7 +599,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
   }
   if (tid == 0) {
     rec.cycles = (uint32_t)(clock64() - S.t_start);
-    atomicAdd(&g_phase_cycles[13 + (rec.layer == BM_LAYER_HQL ? 2 : rec.layer)], (unsigned long long)rec.cycles);
+    if (rec.layer >= BM_LAYER_IDL) atomicAdd(&g_phase_cycles[13 + rec.layer], (unsigned long long)rec.cycles);
     write_record(P, S, rec);
     S.nrec++;
     S.cnt[rec.layer]++;

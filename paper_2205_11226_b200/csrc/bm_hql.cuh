@@ -271,7 +271,35 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
         if (lane > j && lane < n) L[lane * 33 + j] = t * rs;
         __syncwarp();
       }
-      if (lane == 0) H.fail = fail;
+      // identity beyond n
+      for (int j = n; j < 32; j++) {
+        L[lane * 33 + j] = lane == j ? 1.0 : 0.0;
+        if (lane == j) H.rdiag[j] = 1.0;
+      }
+      if (lane >= n)
+        for (int j = 0; j < n; j++) L[lane * 33 + j] = 0.0;
+      __syncwarp();
+      if (lane == 0) {
+        H.fail = fail;
+        atomicAdd(&g_phase_cycles[13], (unsigned long long)(clock64() - ph_t));  // Cholesky alone (diagnostic)
+      }
+      // L^-1 in registers: lane c builds column c by forward substitution
+      // (L rows read as shared-memory broadcasts); identity beyond n
+      double x[32];
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < i; k++) {
+          const double lik = L[i * 33 + k];
+          if (k & 1) s1 = fma(lik, x[k], s1);
+          else s0 = fma(lik, x[k], s0);
+        }
+        const double rdi = H.rdiag[i];
+        x[i] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);
+      }
+#pragma unroll
+      for (int i = 0; i < 32; i++) H.Linv[i * LS + lane] = x[i];
     } else {
       // warps 1..7: Euclidean distances in NumPy's order and the stable
       // k-nearest selection (optimize_alpha, estimators.py:221-223)
@@ -291,34 +319,67 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
         }
       }
       const int k = min(n + 1, m);
-      unsigned taken = 0;
-      for (int it = 0; it < k; it++) {
-        double bv = INFINITY;
-        int bj = 0x7fffffff;
+      // (1) per-thread sort of its PER candidates by (e2, index)
+      int ej[PER];
 #pragma unroll
-        for (int i = 0; i < PER; i++) {
-          const int j = t7 + i * NW7;
-          if (!((taken >> i) & 1u) && (ev[i] < bv || (ev[i] == bv && j < bj))) { bv = ev[i]; bj = j; }
+      for (int i = 0; i < PER; i++) ej[i] = t7 + i * NW7;
+#pragma unroll
+      for (int pass = 0; pass < PER; pass++)
+#pragma unroll
+        for (int i = pass & 1; i + 1 < PER; i += 2) {
+          const bool sw = ev[i + 1] < ev[i] || (ev[i + 1] == ev[i] && ej[i + 1] < ej[i]);
+          if (sw) {
+            const double tv = ev[i];
+            ev[i] = ev[i + 1];
+            ev[i + 1] = tv;
+            const int tj = ej[i];
+            ej[i] = ej[i + 1];
+            ej[i + 1] = tj;
+          }
         }
+      // (2) each warp merges its 32 sorted lanes into its k smallest
+      double* lv = H.R2;                           // [NWARP-1][KMAX] values
+      int* lj = reinterpret_cast<int*>(H.R2 + (NWARP - 1) * KMAX);  // [NWARP-1][KMAX] indices
+      for (int it = 0; it < k; it++) {
+        double bv = ev[0];
+        int bj = ej[0];
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
           const double ov = __shfl_xor_sync(FULL, bv, o);
           const int oj = __shfl_xor_sync(FULL, bj, o);
           if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
         }
-        const int slot = it & 1;
-        if (lane == 0) { H.redmin[slot][w7] = bv; H.redidx[slot][w7] = bj; }
-        asm volatile("bar.sync 1, %0;" ::"r"(NW7) : "memory");  // warps 1..NWARP-1
-        double v = H.redmin[slot][0];
-        int jj = H.redidx[slot][0];
+        if (lane == 0) {
+          lv[w7 * KMAX + it] = bv;
+          lj[w7 * KMAX + it] = bj;
+        }
+        if (ej[0] == bj) {  // pop the winner's head
 #pragma unroll
-        for (int w = 1; w < NWARP - 1; w++)
-          if (H.redmin[slot][w] < v || (H.redmin[slot][w] == v && H.redidx[slot][w] < jj)) {
-            v = H.redmin[slot][w];
-            jj = H.redidx[slot][w];
+          for (int i = 0; i + 1 < PER; i++) {
+            ev[i] = ev[i + 1];
+            ej[i] = ej[i + 1];
           }
-        if ((jj % NW7) == t7) taken |= 1u << (jj / NW7);
-        if (t7 == 0) H.near[it] = jj;
+          ev[PER - 1] = INFINITY;
+          ej[PER - 1] = 0x7fffffff;
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(NW7) : "memory");  // warps 1..NWARP-1
+      // (3) warp 1 merges the NWARP-1 sorted lists: lane w holds list w's head
+      if (w7 == 0) {
+        int ptr = 0;
+        for (int it = 0; it < k; it++) {
+          double bv = (lane < NWARP - 1 && ptr < k) ? lv[lane * KMAX + ptr] : INFINITY;
+          int bj = (lane < NWARP - 1 && ptr < k) ? lj[lane * KMAX + ptr] : 0x7fffffff;
+          const int myj = bj;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) {
+            const double ov = __shfl_xor_sync(FULL, bv, o);
+            const int oj = __shfl_xor_sync(FULL, bj, o);
+            if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
+          }
+          if (lane == 0) H.near[it] = bj;
+          if (myj == bj && lane < NWARP - 1) ptr++;
+        }
       }
     }
     __syncthreads();
@@ -326,26 +387,6 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     if (H.fail) {
       if (tid == 0) out.ok = 0;
       return;
-    }
-    // L^-1 (forward substitution on e_c), identity beyond n: warp w owns
-    // columns w, w+NWARP, ...; LPC = NWARP lanes split each dot product
-    {
-      constexpr int LPC = NWARP;
-      const int c = warp + NWARP * (lane / LPC), sub = lane % LPC;
-      for (int i = 0; i < 32; i++) {
-        double s = 0.0;
-        if (i < n && i > c)
-          for (int k = c + sub; k < i; k += LPC) s = fma(L[i * 33 + k], H.Linv[k * LS + c], s);
-#pragma unroll
-        for (int o = 1; o < LPC; o <<= 1) s += __shfl_xor_sync(FULL, s, o);
-        double x;
-        if (i < c) x = 0.0;
-        else if (i >= n) x = (i == c) ? 1.0 : 0.0;
-        else if (i == c) x = H.rdiag[i];
-        else x = -s * H.rdiag[i];
-        if (sub == 0) H.Linv[i * LS + c] = x;
-        __syncwarp();
-      }
     }
     __syncthreads();
     BM_PHASE(4);

@@ -303,8 +303,8 @@ def conceal_image(
     require_same_shape(pixels, states)
     torch = _native.require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device())
-    px = torch.from_numpy(np.ascontiguousarray(pixels, dtype=np.float64)).to(dev, non_blocking=False)
-    st = torch.from_numpy(np.ascontiguousarray(states, dtype=np.uint8)).to(dev)
+    px = torch.from_numpy(np.array(pixels, dtype=np.float64, copy=True)).to(dev)
+    st = torch.from_numpy(np.array(states, dtype=np.uint8, copy=True)).to(dev)
     t0 = time.perf_counter()
     res = conceal_batch(px, st, profile, sigma2=sigma2, forced_layer=forced_layer, want_u8=False,
                         want_f64=True, records=True)
