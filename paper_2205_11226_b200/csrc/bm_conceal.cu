@@ -533,7 +533,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         if (tid == 0) atomicAdd(&g_phase_cycles[0], (unsigned long long)(clock64() - S.t_start));
         hql_columns(S.hql, E.n, E.uoff);
         __syncthreads();
-        ZView zv{S.tile, S.cand};
+        TileLoader zv{smem_addr(S.tile), S.cand};
         hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout);
         __syncthreads();
         if (S.hout.ok) {
@@ -889,7 +889,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
   int layer = BM_LAYER_BRL, fallback = 0;
   bool done = false;
   if (A.layer == BM_LAYER_HQL && m >= 2) {
-    ZView zv{Z, nullptr};
+    DenseLoader zv{Z};
     hql_mma(zv, m, n, E.y0, S.hql, gs, S.hout);
     __syncthreads();
     if (S.hout.ok) {

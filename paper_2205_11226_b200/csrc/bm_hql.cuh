@@ -25,14 +25,19 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-// Z view: column col of candidate j is ptr[base(j) + coff[col]] (coff >= 0) or
-// the constant cconst[col].  Columns: 0..31 = y (N_y used, rest 0), 32..35 = x,
-// 36 = 1 (sums), 37..39 = 0.
-struct ZView {
-  const double* ptr;
-  const uint16_t* cand;  // tile positions (fused kernel) or nullptr (dense, stride 40)
-  __device__ __forceinline__ int base(int j) const { return cand ? (int)cand[j] : j * 40; }
+// Candidate loaders.  Column col of candidate j: columns 0..31 = y (N_y used,
+// rest 0), 32..35 = x, 36 = 1 (sums), 37..39 = 0.  A lane resolves its
+// columns once into ColRefs; a fragment element is then one IMAD + one load.
+struct ColRef {
+  uint32_t addr, mul;
 };
+
+__device__ __forceinline__ double ld_shared_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 constexpr int LS = 36;  // stride of Linv / Vn: conflict-free A-fragment loads (36 = 4 mod 16)
 
@@ -71,10 +76,6 @@ constexpr size_t HQL_Z = HQL_E2 + MAXCAND;                   // dense Z [MAXCAND
 constexpr size_t HQL_SCRATCH_FUSED = HQL_Z;
 constexpr size_t HQL_SCRATCH_DENSE = HQL_Z + (size_t)MAXCAND * 40;
 
-__device__ __forceinline__ double zval(const double* ptr, int b, int off, double cst) {
-  return off >= 0 ? ptr[b + off] : cst;
-}
-
 // Fixed-order tree reduction of per-warp register tiles (NWARP warps -> warp 0);
 // red must hold (NWARP/2) * N * 32 doubles.
 template <int N>
@@ -94,6 +95,26 @@ __device__ __forceinline__ void tree_reduce(double (&acc)[N], double* red) {
     }
   }
 }
+
+// Fused kernel: candidates are window origins cand[j] in the shared support tile.
+struct TileLoader {
+  uint32_t tile_s;       // shared address of tile[0]
+  const uint16_t* cand;  // shared
+  __device__ __forceinline__ int base(int j) const { return cand[j]; }
+  __device__ __forceinline__ ColRef ref(const HqlSmem& H, int col) const {
+    const int off = H.coff[col];
+    return off >= 0 ? ColRef{tile_s + 8u * (uint32_t)off, 8u} : ColRef{smem_addr(&H.cconst[col]), 0u};
+  }
+  __device__ __forceinline__ double at(const ColRef& r, int b) const { return ld_shared_f64(r.addr + (uint32_t)b * r.mul); }
+};
+
+// Estimator API: dense Z [m][40] in global memory (all 40 columns stored).
+struct DenseLoader {
+  const double* Z;
+  __device__ __forceinline__ int base(int j) const { return j * 40; }
+  __device__ __forceinline__ ColRef ref(const HqlSmem&, int col) const { return ColRef{(uint32_t)col, 1u}; }
+  __device__ __forceinline__ double at(const ColRef& r, int b) const { return Z[(size_t)b * r.mul + r.addr]; }
+};
 
 // Column table of the Z view for target layout n (uoff: tile offsets of the
 // n usable context positions; nullptr for the dense layout).
@@ -133,7 +154,8 @@ struct HqlOut {
   int ok;
 };
 
-__device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem& H, double* __restrict__ gs,
+template <class ZL>
+__device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H, double* __restrict__ gs,
                         HqlOut& out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
@@ -146,12 +168,11 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
   // ---------------------------------------------------------------- means
   {
     double a0 = 0.0, a1 = 0.0;
-    const int off0 = H.coff[lane], off1 = lane < 8 ? H.coff[32 + lane] : -1;
-    const double c0 = H.cconst[lane], c1 = lane < 8 ? H.cconst[32 + lane] : 0.0;
+    const ColRef c0 = zv.ref(H, lane), c1 = zv.ref(H, lane < 8 ? 32 + lane : 37);
     for (int j = warp; j < m; j += NWARP) {
       const int b = zv.base(j);
-      a0 += zval(zv.ptr, b, off0, c0);
-      a1 += zval(zv.ptr, b, off1, c1);
+      a0 += zv.at(c0, b);
+      a1 += zv.at(c1, b);
     }
     H.wmin[warp][lane] = a0;
     if (lane < 8) H.wmin[warp][32 + lane] = a1;
@@ -168,13 +189,12 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
 
   // ------------------------------------------------- covariance (DMMA)
   {
-    int off[5];
-    double cst[5], mu[5];
+    ColRef cr[5];
+    double mu[5];
 #pragma unroll
     for (int tl = 0; tl < 5; tl++) {
       const int col = 8 * tl + g;
-      off[tl] = H.coff[col];
-      cst[tl] = H.cconst[col];
+      cr[tl] = zv.ref(H, col);
       mu[tl] = H.mean[col];
     }
     double acc[28];
@@ -184,10 +204,13 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     double f[5], fn[5];
     auto load_f = [&](int s, double(&o)[5]) {
       const int j = 4 * s + t4;
-      const bool valid = s < nks && j < m;
-      const int b = valid ? zv.base(j) : 0;
+      const bool valid = j < m;
+      const int b = zv.base(min(j, m - 1));  // clamped: branch-free loads
 #pragma unroll
-      for (int tl = 0; tl < 5; tl++) o[tl] = valid ? zval(zv.ptr, b, off[tl], cst[tl]) - mu[tl] : 0.0;
+      for (int tl = 0; tl < 5; tl++) {
+        const double v = zv.at(cr[tl], b) - mu[tl];
+        o[tl] = valid ? v : 0.0;
+      }
     };
     load_f(warp, f);
 #pragma unroll 1
@@ -244,33 +267,45 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
         for (int i = 0; i < n; i++) cyy[i * 33 + i] += ridge;
       }
       __syncwarp();
+      // Blocked right-looking Cholesky (8-column blocks) on warp 0: within a
+      // block, lanes are rows and dot products run over the block's columns
+      // only; the trailing update applies the block's rank-8 correction.
       bool fail = false;
-      for (int j = 0; j < n; j++) {
-        double t = 0.0;
-        if (lane >= j && lane < n) {
-          const double* Li = L + lane * 33;
-          const double* Lj = L + j * 33;
-          double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-          int k = 0;
-          for (; k + 4 <= j; k += 4) {
-            t0 = fma(Li[k], Lj[k], t0);
-            t1 = fma(Li[k + 1], Lj[k + 1], t1);
-            t2 = fma(Li[k + 2], Lj[k + 2], t2);
-            t3 = fma(Li[k + 3], Lj[k + 3], t3);
+      for (int c0 = 0; c0 < n && !fail; c0 += 8) {
+        const int c1 = min(n, c0 + 8);
+        for (int j = c0; j < c1; j++) {
+          double t = 0.0;
+          if (lane >= j && lane < n) {
+            t = cyy[lane * 33 + j];
+            for (int k = c0; k < j; k++) t = fma(-L[lane * 33 + k], L[j * 33 + k], t);
           }
-          for (; k < j; k++) t0 = fma(Li[k], Lj[k], t0);
-          t = cyy[lane * 33 + j] - ((t0 + t1) + (t2 + t3));
+          const double sd = __shfl_sync(FULL, t, j);
+          if (!(sd > 0.0)) { fail = true; break; }
+          const double rs = rsqrt(sd);  // 1 / L_jj
+          if (lane == j) {
+            L[j * 33 + j] = sd * rs;
+            H.rdiag[j] = rs;
+          }
+          if (lane > j && lane < n) L[lane * 33 + j] = t * rs;
+          __syncwarp();
         }
-        const double sd = __shfl_sync(FULL, t, j);
-        if (!(sd > 0.0)) { fail = true; break; }
-        const double rs = rsqrt(sd);  // 1 / L_jj
-        if (lane == j) {
-          L[j * 33 + j] = sd * rs;
-          H.rdiag[j] = rs;
+        if (fail) break;
+        // trailing update A[i][jj] -= sum_{k in block} L[i][k] L[jj][k], c1 <= jj <= i < n
+        const int rem = n - c1;
+        for (int e = lane; e < rem * rem; e += 32) {
+          const int i = c1 + e / rem, jj = c1 + e % rem;
+          if (jj > i) continue;
+          double t = cyy[i * 33 + jj];
+#pragma unroll
+          for (int k = 0; k < 8; k++)
+            if (c0 + k < c1) t = fma(-L[i * 33 + c0 + k], L[jj * 33 + c0 + k], t);
+          cyy[i * 33 + jj] = t;
         }
-        if (lane > j && lane < n) L[lane * 33 + j] = t * rs;
         __syncwarp();
       }
+      // the factor's lower triangle is complete; clear the upper part
+      for (int j = 0; j < n; j++)
+        if (lane < j) L[lane * 33 + j] = 0.0;
       // identity beyond n
       for (int j = n; j < 32; j++) {
         L[lane * 33 + j] = lane == j ? 1.0 : 0.0;
@@ -314,7 +349,7 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
           const int b = zv.base(j);
           double v[32];
 #pragma unroll
-          for (int t = 0; t < 32; t++) v[t] = t < n ? zv.ptr[b + H.coff[t]] - y0[t] : 0.0;
+          for (int t = 0; t < 32; t++) v[t] = t < n ? zv.at(zv.ref(H, t), b) - y0[t] : 0.0;
           ev[i] = pairwise_sq32(v, n);
         }
       }
@@ -402,22 +437,22 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
   // ------------------------------------- V = L^-1 (y0 - Y)^T and d (DMMA)
   {
     double y0r[8];
-    int offy[8];
+    ColRef ry[8];
 #pragma unroll
     for (int kk = 0; kk < 8; kk++) {
       const int dim = 4 * kk + t4;
       y0r[kk] = dim < n ? y0[dim] : 0.0;
-      offy[kk] = H.coff[dim];
+      ry[kk] = zv.ref(H, dim);
     }
     double fb[8], fbn[8];
     auto load_v = [&](int c, double(&o)[8]) {
       const int jB = 8 * c + g;
-      const bool vb = c < nct && jB < m;
-      const int bB = vb ? zv.base(jB) : 0;
+      const bool vb = jB < m;
+      const int bB = zv.base(min(jB, m - 1));
 #pragma unroll
       for (int kk = 0; kk < 8; kk++) {
-        const int dim = 4 * kk + t4;
-        o[kk] = (vb && dim < n) ? y0r[kk] - zv.ptr[bB + offy[kk]] : 0.0;
+        const double v = y0r[kk] - zv.at(ry[kk], bB);  // y0r = 0 and column 0 beyond n
+        o[kk] = vb ? v : 0.0;
       }
     };
     load_v(warp, fb);
@@ -476,13 +511,9 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
   }
 
   // ------------------------------------------------ beta grid (DMMA)
-  int offz[5];
-  double cstz[5];
+  ColRef crz[5];
 #pragma unroll
-  for (int ct = 0; ct < 5; ct++) {
-    offz[ct] = H.coff[8 * ct + g];
-    cstz[ct] = H.cconst[8 * ct + g];
-  }
+  for (int ct = 0; ct < 5; ct++) crz[ct] = zv.ref(H, 8 * ct + g);
   {
     // MMA row 8r+g holds grid point beta_(3g+r): a lane's three betas are
     // consecutive, so one exp at beta_(3g+2) and two squarings give all three
@@ -496,11 +527,13 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
     double dl, dln, fb[5], fbn[5];
     auto load_b = [&](int s, double& d, double(&o)[5]) {
       const int j = 4 * s + t4;
-      const bool valid = s < nks && j < m;
-      const int b = valid ? zv.base(j) : 0;
-      d = valid ? dmin - gD[j] : -INFINITY;  // -inf -> weight 0 for padding
+      const bool valid = j < m;
+      const int jc = min(j, m - 1);
+      const int b = zv.base(jc);
+      const double dd = dmin - gD[jc];
+      d = valid ? dd : -INFINITY;  // -inf -> weight 0 for padding
 #pragma unroll
-      for (int ct = 0; ct < 5; ct++) o[ct] = valid ? zval(zv.ptr, b, offz[ct], cstz[ct]) : 0.0;
+      for (int ct = 0; ct < 5; ct++) o[ct] = zv.at(crz[ct], b);  // weight 0 for padding
     };
     load_b(warp, dl, fb);
 #pragma unroll 1
@@ -629,10 +662,9 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
 #pragma unroll
       for (int ks = 0; ks < 2; ks++) {
         const int j = 8 * c + 4 * ks + t4;
-        const bool valid = j < m;
-        const int b = valid ? zv.base(j) : 0;
+        const int b = zv.base(min(j, m - 1));  // padding columns get weight 0
 #pragma unroll
-        for (int ct = 0; ct < 5; ct++) fz[ks][ct] = valid ? zval(zv.ptr, b, offz[ct], cstz[ct]) : 0.0;
+        for (int ct = 0; ct < 5; ct++) fz[ks][ct] = zv.at(crz[ct], b);
       }
 #pragma unroll
       for (int rr = 0; rr < RR; rr++) {
@@ -718,7 +750,7 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       const double S = Zp[i * 40 + 36];
       double s = 0.0;
       for (int q = 0; q <= t && q < n; q++) {
-        const double r = zv.ptr[b + H.coff[q]] - Zp[i * 40 + q] / S;  // y_i - y~_i
+        const double r = zv.at(zv.ref(H, q), b) - Zp[i * 40 + q] / S;  // y_i - y~_i
         s = fma(H.Linv[t * LS + q], r, s);
       }
       u[i * 32 + t] = t < n ? s : 0.0;
@@ -731,7 +763,7 @@ __device__ void hql_mma(const ZView& zv, int m, int n, const double* y0, HqlSmem
       const int b = zv.base(H.near[i]);
       const double S = Zp[i * 40 + 36];
       H.cmat[q * k + i] = c;
-      H.rmat[q * k + i] = zval(zv.ptr, b, H.coff[32 + q], 0.0) - Zp[i * 40 + 32 + q] / S;
+      H.rmat[q * k + i] = zv.at(zv.ref(H, 32 + q), b) - Zp[i * 40 + 32 + q] / S;
     }
     __syncthreads();
     if (warp == 0) {
