@@ -65,9 +65,11 @@ struct CellSmem {
   uint64_t lostbits[TILE];
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
-  float rbuf[2 * NT];
-  int pref[2 * NT];
+  float rbuf[MAXCAND];   // per expansion-map entry: nu weight, -1 = not admissible
+  int pref[2];
   int wcnt[2 * NWARP];
+  double ringsum[MAXRING + 2];
+  int ringcnt[MAXRING + 2];
   int ring_off[MAXRING + 2];
   // per-patch control (written by warp 0 / thread 0, read after a barrier)
   int ticket, slot, f, gr, gc;
@@ -155,23 +157,27 @@ __global__ void k_slots(KParams P, const int* flags, const int* excl) {
   }
 }
 
-// Longest-path level of every lost cell in its frame's dependency DAG:
-// level(u) = 1 + max level of its lost earlier-raster 8-neighbours
-// ((r-1,c-1),(r-1,c),(r-1,c+1),(r,c-1)); one warp per frame, rows in order,
-// the left-neighbour chain inside a row as a max-plus warp scan.
-__global__ void k_levels(KParams P) {
+// Longest-path depth of every lost cell in its frame's dependency DAG, one
+// warp per frame.  REV = false: level(u) = 1 + max level of its lost
+// earlier-raster 8-neighbours ((r-1,c-1),(r-1,c),(r-1,c+1),(r,c-1)), rows top
+// down.  REV = true: the mirrored recurrence over later-raster neighbours
+// gives height(u) - 1 (longest chain of dependants).  The left-neighbour
+// chain inside a row is a max-plus segmented warp scan.
+template <bool REV>
+__global__ void k_depth(KParams P, unsigned* out) {
   const int lane = threadIdx.x & 31;
   const int f = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (f >= P.B) return;
   const int GR = P.GR, GC = P.GC;
   const int* sm = P.slotmap + (size_t)f * GR * GC;
+  auto slot_at = [&](int r, int c) { return sm[(REV ? GR - 1 - r : r) * GC + (REV ? GC - 1 - c : c)]; };
   unsigned maxlvl = 0;
   for (int r = 0; r < GR; r++) {
-    int carry = -1000000;  // level(c-1) - (c-1) style carry across chunks: stores level of the cell left of chunk
+    int carry = -1000000;
     int left_lost = 0;
     for (int c0 = 0; c0 < GC; c0 += 32) {
       const int c = c0 + lane;
-      int slot = c < GC ? sm[r * GC + c] : -1;
+      const int slot = c < GC ? slot_at(r, c) : -1;
       int base = -1;  // -1: not lost
       if (slot >= 0) {
         int b = 0;
@@ -179,23 +185,20 @@ __global__ void k_levels(KParams P) {
           for (int dc = -1; dc <= 1; dc++) {
             const int cc = c + dc;
             if (cc < 0 || cc >= GC) continue;
-            const int s2 = sm[(r - 1) * GC + cc];
-            if (s2 >= 0) b = max(b, (int)P.level[s2] + 1);
+            const int s2 = slot_at(r - 1, cc);
+            if (s2 >= 0) b = max(b, (int)out[s2] + 1);
           }
         }
         base = b;
       }
-      // chain: level(c) = max(base(c), level(c-1)+1) when c-1 is lost.
-      // value(c) = level(c) - c; run-segmented prefix max of (base - c).
+      // chain: depth(c) = max(base(c), depth(c-1)+1) when c-1 is lost;
+      // value(c) = depth(c) - c; run-segmented prefix max of (base - c).
       const bool lost = slot >= 0;
       int val = lost ? base - c : -1000000;
-      // segment starts where the left neighbour is not lost
       const int up_lost = __shfl_up_sync(FULL, (int)lost, 1);
       const bool prev_lost_inchunk = lane > 0 ? up_lost : left_lost;
       int seg_start = lost && !prev_lost_inchunk;
-      // incorporate carry from previous chunk for lane 0 when left neighbour lost
       if (lane == 0 && lost && left_lost) val = max(val, carry);
-      // inclusive segmented max-scan
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int ov = __shfl_up_sync(FULL, val, o);
@@ -207,7 +210,7 @@ __global__ void k_levels(KParams P) {
       }
       if (lost) {
         const unsigned lv = (unsigned)(val + c);
-        P.level[slot] = lv;
+        out[slot] = lv;
         maxlvl = max(maxlvl, lv);
       }
       carry = __shfl_sync(FULL, val, 31);
@@ -218,7 +221,16 @@ __global__ void k_levels(KParams P) {
     __threadfence_block();
   }
   maxlvl = (unsigned)__reduce_max_sync(FULL, maxlvl);
-  if (lane == 0) atomicMax((unsigned long long*)&P.counters[7], (unsigned long long)maxlvl);
+  if (!REV && lane == 0) atomicMax((unsigned long long*)&P.counters[7], (unsigned long long)maxlvl);
+}
+
+// Ticket order key: longest chain of dependants first (critical-path
+// priority; a topological order, since a cell's dependants have smaller
+// heights), then level.  Invalid slots (>= nslots) sort last.
+__global__ void k_keys(const unsigned* level, const unsigned* height, const int* nslots, unsigned* key, int n) {
+  const int ns = *nslots;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    key[i] = i < ns ? ((0xFFFFu - min(height[i], 0xFFFEu)) << 16) | min(level[i], 0xFFFFu) : 0xFFFFFFFFu;
 }
 
 __global__ void k_iota(unsigned* v, const int* nslots, int n) {
@@ -268,6 +280,95 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
 // by ring nu gate (profiles.py:113-124, framework.py:171-207), or the one-shot
 // full gather of _forced_estimate (profiles.py:148-149).  Sets S.m, rings_used,
 // nu; S.cand holds the candidates.
+// Screen entries [e0, e0 + GCH) of the expansion map: admissibility
+// (framework.py:176), FP32 nu weight in gated mode (raw_idl_weights,
+// estimators.py:105-109), ordered ballot compaction into S.cand after the
+// m_total candidates already gathered.  r is stored per entry in S.rbuf
+// (-1 = not admissible).  Returns the chunk's admissible count (all threads).
+constexpr int GH = 2, GCH = GH * NT;  // entries per chunk: GH per thread
+__device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
+                                            int C0, bool gated, float invf) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  EstSmem& E = S.est;
+  const int n = E.n;
+  bool adm[GH];
+  int pos[GH];
+#pragma unroll
+  for (int h = 0; h < GH; h++) {
+    const int e = e0 + h * NT + tid;
+    adm[h] = false;
+    pos[h] = 0;
+    float rw = -1.f;
+    if (e < K) {
+      // ring of entry e: binary search over the ring offsets
+      int lo = 1, hi = max_ring;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (S.ring_off[mid] <= e) lo = mid;
+        else hi = mid - 1;
+      }
+      int a, b;
+      ring_entry(g, lo, e - S.ring_off[lo], a, b);
+      const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < 6; q++)
+        if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) ok = false;
+      adm[h] = ok;
+      if (ok) {
+        pos[h] = wr * TS + wc;
+        rw = 0.f;
+        if (gated) {
+          // nu screening: FP32 Nadaraya-Watson distance + weight
+          const float* tp = S.tile32 + pos[h];
+          float d2a = 0.f, d2b = 0.f;
+          int k = 0;
+          for (; k + 2 <= n; k += 2) {
+            const float da = tp[E.uoff[k]] - E.y0f[k];
+            const float db = tp[E.uoff[k + 1]] - E.y0f[k + 1];
+            d2a = fmaf(da, da, d2a);
+            d2b = fmaf(db, db, d2b);
+          }
+          if (k < n) {
+            const float da = tp[E.uoff[k]] - E.y0f[k];
+            d2a = fmaf(da, da, d2a);
+          }
+          rw = expf(-(d2a + d2b) * invf);
+        }
+      }
+      S.rbuf[e] = rw;
+    }
+    const unsigned bal = __ballot_sync(FULL, adm[h]);
+    if (lane == 0) S.wcnt[h * NWARP + warp] = __popc(bal);
+  }
+  __syncthreads();
+  // ordered compaction (entries are in (h, warp, lane) = expansion-map order)
+  const int m0 = S.m_total;
+  int tot = 0;
+#pragma unroll
+  for (int h = 0; h < GH; h++) {
+    int base = tot;
+#pragma unroll
+    for (int w = 0; w < NWARP; w++) {
+      if (w < warp) base += S.wcnt[h * NWARP + w];
+      tot += S.wcnt[h * NWARP + w];
+    }
+    const unsigned bal = __ballot_sync(FULL, adm[h]);
+    const int wpre = __popc(bal & ((1u << lane) - 1));
+    if (adm[h]) S.cand[m0 + base + wpre] = (uint16_t)pos[h];
+  }
+  __syncthreads();
+  if (tid == 0) S.m_total = m0 + tot;
+  return tot;
+}
+
+// Gather of the admissible candidates in (ring, row, col) order with the ring
+// by ring nu gate (profiles.py:113-124, framework.py:171-207), or the one-shot
+// full gather of _forced_estimate (profiles.py:148-149).  Sets S.m, rings_used,
+// nu; S.cand holds the candidates.  The gate walks the first chunk (rings
+// 1..~5, where IDL decisions fall) ring by ring; if nu has not reached T_nu
+// the rest of the map is screened in one barrier-light sweep and the per-ring
+// sums are formed afterwards, giving the same stopping ring.
 __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool gated) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
@@ -285,30 +386,27 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   g.B0 = c0 + 2;
   g.B1 = c1 - 4;
   if (warp == 0) {
-    int cnt = (lane >= 1 && lane <= 26) ? ring_count(g, lane) : 0;
-    // inclusive scan
+    const int cnt = (lane >= 1 && lane <= 26) ? ring_count(g, lane) : 0;
     int inc = cnt;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int v = __shfl_up_sync(FULL, inc, o);
+      const int v = __shfl_up_sync(FULL, inc, o);
       if (lane >= o) inc += v;
     }
-    // ring_off[r] = sum of counts of rings < r
-    if (lane <= 27) S.ring_off[lane] = inc - cnt;  // lane 0 -> 0
-    unsigned nz = __ballot_sync(FULL, cnt > 0);
-    if (lane == 0) {
-      S.max_ring = nz ? 31 - __clz(nz) : 0;
-      S.K = S.ring_off[0] + 0;
-    }
+    if (lane <= 27) S.ring_off[lane] = inc - cnt;  // ring_off[r] = entries of rings < r
+    const unsigned nz = __ballot_sync(FULL, cnt > 0);
+    const int mr = nz ? 31 - __clz(nz) : 0;
+    const int K = __shfl_sync(FULL, inc, mr);
     __syncwarp();
     if (lane == 0) {
-      S.K = S.max_ring ? S.ring_off[S.max_ring] + ring_count(g, S.max_ring) : 0;
-      S.ring_off[S.max_ring + 1] = S.K;
+      S.max_ring = mr;
+      S.K = mr ? K : 0;
+      S.ring_off[mr + 1] = S.K;
       S.m = 0;
       S.m_total = 0;
       S.nu = 0.0;
       S.carry = 0.0;
-      S.cur_ring = 0;  // rings fully accounted
+      S.cur_ring = 0;
       S.gated_stop = 0;
       S.rings_used = 0;
     }
@@ -321,118 +419,94 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     return;
   }
   const float invf = (float)(1.0 / (2.0 * P.sigma2 * n));
-  constexpr int GH = 2, GCH = GH * NT;  // entries per chunk: GH per thread
-  for (int e0 = 0; e0 < K; e0 += GCH) {
-    bool adm[GH];
-    int pos[GH];
-#pragma unroll
-    for (int h = 0; h < GH; h++) {
-      const int e = e0 + h * NT + tid;
-      adm[h] = false;
-      pos[h] = 0;
-      float rw = 0.f;
-      if (e < K) {
-        int r = 1;
-        while (r < max_ring && S.ring_off[r + 1] <= e) r++;
-        int a, b;
-        ring_entry(g, r, e - S.ring_off[r], a, b);
-        const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
-        bool ok = true;
-#pragma unroll
-        for (int q = 0; q < 6; q++)
-          if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) ok = false;
-        adm[h] = ok;
-        if (ok) {
-          pos[h] = wr * TS + wc;
-          if (gated) {
-            // nu screening: FP32 Nadaraya-Watson distance + weight
-            // (raw_idl_weights, estimators.py:105-109)
-            const float* tp = S.tile32 + pos[h];
-            float d2a = 0.f, d2b = 0.f;
-            int k = 0;
-            for (; k + 2 <= n; k += 2) {
-              const float da = tp[E.uoff[k]] - E.y0f[k];
-              const float db = tp[E.uoff[k + 1]] - E.y0f[k + 1];
-              d2a = fmaf(da, da, d2a);
-              d2b = fmaf(db, db, d2b);
-            }
-            if (k < n) {
-              const float da = tp[E.uoff[k]] - E.y0f[k];
-              d2a = fmaf(da, da, d2a);
-            }
-            rw = expf(-(d2a + d2b) * invf);
-          }
-        }
-      }
-      const unsigned bal = __ballot_sync(FULL, adm[h]);
-      if (lane == 0) S.wcnt[h * NWARP + warp] = __popc(bal);
-      S.rbuf[h * NT + tid] = adm[h] ? rw : 0.f;
+  if (!gated) {
+    for (int e0 = 0; e0 < K; e0 += GCH) screen_chunk(S, g, e0, K, max_ring, R0, C0, false, invf);
+    if (tid == 0) {
+      S.m = S.m_total;
+      S.rings_used = max_ring;
     }
     __syncthreads();
-    // ordered compaction (entries are in (h, warp, lane) = expansion-map order)
-    const int m0 = S.m_total;
-    int tot = 0;
-#pragma unroll
-    for (int h = 0; h < GH; h++) {
-      int base = tot;
-#pragma unroll
-      for (int w = 0; w < NWARP; w++) {
-        if (w < warp) base += S.wcnt[h * NWARP + w];
-        tot += S.wcnt[h * NWARP + w];
-      }
-      const unsigned bal = __ballot_sync(FULL, adm[h]);
-      const int wpre = __popc(bal & ((1u << lane) - 1));
-      if (adm[h]) S.cand[m0 + base + wpre] = (uint16_t)pos[h];
-      S.pref[h * NT + tid] = base + wpre + (adm[h] ? 1 : 0);  // inclusive count up to e
-    }
-    __syncthreads();
-    if (!gated) {
-      if (tid == 0) S.m_total = m0 + tot;
-      __syncthreads();
-      continue;
-    }
-    // nu bookkeeping, ring by ring (warp 0)
-    if (warp == 0) {
-      const int e1 = min(e0 + GCH, K);
-      int r = S.cur_ring + 1;
-      double carry = S.carry, nu = S.nu;
-      int stop = 0;
-      while (r <= max_ring) {
-        const int lo = max(S.ring_off[r], e0), hi = min(S.ring_off[r + 1], e1);
-        double part = 0.0;
-        for (int i = lo + lane; i < hi; i += 32) part += (double)S.rbuf[i - e0];
-        part = warp_sum(part);
-        if (S.ring_off[r + 1] > e1) {  // ring continues in the next chunk
-          carry += part;
-          break;
-        }
-        nu += carry + part;  // nu += sum of the ring's raw weights
-        carry = 0.0;
-        if (!(nu < P.t_nu) || r >= max_ring) {
-          stop = 1;
-          if (lane == 0) {
-            S.rings_used = r;
-            const int end = S.ring_off[r + 1];
-            S.m = m0 + (end > e0 ? S.pref[end - e0 - 1] : 0);
-          }
-          break;
-        }
-        r++;
-      }
-      if (lane == 0) {
-        S.cur_ring = stop ? r : r - 1;
-        S.carry = carry;
-        S.nu = nu;
-        S.gated_stop = stop;
-        S.m_total = m0 + tot;
-      }
-    }
-    __syncthreads();
-    if (S.gated_stop) break;
+    return;
   }
-  if (!gated && tid == 0) {
-    S.m = S.m_total;
-    S.rings_used = max_ring;
+  // ---- first chunk, ring by ring
+  const int e1 = min(GCH, K);
+  screen_chunk(S, g, 0, K, max_ring, R0, C0, true, invf);
+  if (warp == 0) {
+    double nu = 0.0, carry = 0.0;
+    int cnt_done = 0, stop = 0, r = 1;
+    for (; r <= max_ring; r++) {
+      const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
+      double part = 0.0;
+      int c = 0;
+      for (int i = lo + lane; i < hi; i += 32) {
+        const float v = S.rbuf[i];
+        if (v >= 0.f) {
+          part += (double)v;
+          c++;
+        }
+      }
+      part = warp_sum(part);
+      c = warp_sumi(c);
+      cnt_done += c;
+      if (S.ring_off[r + 1] > e1) {  // ring continues past the first chunk
+        carry = part;
+        break;
+      }
+      nu += part;  // nu += sum of the ring's raw weights (profiles.py:122)
+      if (!(nu < P.t_nu) || r >= max_ring) {
+        stop = 1;
+        break;
+      }
+    }
+    if (lane == 0) {
+      S.gated_stop = stop;
+      S.nu = nu;
+      S.carry = carry;
+      S.cur_ring = r;  // stop ring, or the ring straddling the chunk end
+      if (stop) {
+        S.rings_used = r;
+        S.m = cnt_done;
+      }
+      S.pref[0] = cnt_done;  // admissible entries of completed rings
+    }
+  }
+  __syncthreads();
+  if (S.gated_stop) return;
+  // ---- rest of the map in one sweep, then ring sums and the stopping ring
+  for (int e0 = GCH; e0 < K; e0 += GCH) screen_chunk(S, g, e0, K, max_ring, R0, C0, true, invf);
+  const int rs = S.cur_ring;  // first ring not yet accounted (may have a carry)
+  for (int r = rs + warp; r <= max_ring; r += NWARP) {
+    const int lo = max(S.ring_off[r], r == rs ? e1 : 0), hi = S.ring_off[r + 1];
+    double part = 0.0;
+    int c = 0;
+    for (int i = lo + lane; i < hi; i += 32) {
+      const float v = S.rbuf[i];
+      if (v >= 0.f) {
+        part += (double)v;
+        c++;
+      }
+    }
+    part = warp_sum(part);
+    c = warp_sumi(c);
+    if (lane == 0) {
+      S.ringsum[r] = part;
+      S.ringcnt[r] = c;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double nu = S.nu;
+    int m = S.pref[0];
+    int r = rs;
+    for (; r <= max_ring; r++) {
+      const double ring = (r == rs ? S.carry : 0.0) + S.ringsum[r];
+      m += S.ringcnt[r];
+      nu += ring;
+      if (!(nu < P.t_nu) || r >= max_ring) break;
+    }
+    S.nu = nu;
+    S.rings_used = r;
+    S.m = m;
   }
   __syncthreads();
 }
@@ -533,7 +607,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         if (tid == 0) atomicAdd(&g_phase_cycles[0], (unsigned long long)(clock64() - S.t_start));
         hql_columns(S.hql, E.n, E.uoff);
         __syncthreads();
-        TileLoader zv{smem_addr(S.tile), S.cand};
+        TileLoader zv{S.tile, S.cand};
         hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout);
         __syncthreads();
         if (S.hout.ok) {
@@ -949,7 +1023,7 @@ namespace {
 
 struct Layout {
   size_t ncell;
-  size_t off_slotmap, off_slot_cell, off_level, off_level2, off_order, off_order_in, off_done, off_nslots,
+  size_t off_slotmap, off_slot_cell, off_level, off_level2, off_height, off_keys, off_order, off_order_in, off_done, off_nslots,
       off_ticket, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_cub, cub_bytes, off_scratch,
       scratch_per_cta, total;
   int grid;
@@ -999,6 +1073,8 @@ Layout layout(const bm_params* p) {
   L.off_slot_cell = o; o = align_up(o + nc * 4);
   L.off_level = o; o = align_up(o + nc * 4);
   L.off_level2 = o; o = align_up(o + nc * 4);
+  L.off_height = o; o = align_up(o + nc * 4);
+  L.off_keys = o; o = align_up(o + nc * 4);
   L.off_order = o; o = align_up(o + nc * 4);
   L.off_order_in = o; o = align_up(o + nc * 4);
   L.off_done = o; o = align_up(o + nc * 4);
@@ -1150,14 +1226,15 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
     if ((e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cb, flags, excl, nc, stream)) != cudaSuccess)
       return cuda_status(e);
     k_slots<<<sms * 4, 256, 0, stream>>>(P, flags, excl);
-    // invalid slots (>= nslots) keep the max key so they sort last
-    if ((e = cudaMemsetAsync(P.level, 0xff, (size_t)nc * 4, stream)) != cudaSuccess) return cuda_status(e);
-    k_levels<<<(P.B + 7) / 8, 256, 0, stream>>>(P);
-    // ticket order: slots sorted by level (stable -> frame, raster within a level)
+    unsigned* height = (unsigned*)(ws + L.off_height);
+    unsigned* keys = (unsigned*)(ws + L.off_keys);
+    k_depth<false><<<(P.B + 7) / 8, 256, 0, stream>>>(P, P.level);
+    k_depth<true><<<(P.B + 7) / 8, 256, 0, stream>>>(P, height);
+    k_keys<<<sms, 256, 0, stream>>>(P.level, height, P.nslots, keys, nc);
+    // ticket order: slots sorted by (height desc, level) (stable -> frame, raster)
     k_iota<<<sms, 256, 0, stream>>>((unsigned*)(ws + L.off_order_in), P.nslots, nc);
-    // slots beyond nslots carry garbage levels: give them the max key
     cb = L.cub_bytes;
-    if ((e = cub::DeviceRadixSort::SortPairs(ws + L.off_cub, cb, P.level, (unsigned*)(ws + L.off_level2),
+    if ((e = cub::DeviceRadixSort::SortPairs(ws + L.off_cub, cb, keys, (unsigned*)(ws + L.off_level2),
                                              (unsigned*)(ws + L.off_order_in), P.order, nc, 0, 32, stream)) !=
         cudaSuccess)
       return cuda_status(e);

@@ -29,7 +29,8 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 // rest 0), 32..35 = x, 36 = 1 (sums), 37..39 = 0.  A lane resolves its
 // columns once into ColRefs; a fragment element is then one IMAD + one load.
 struct ColRef {
-  uint32_t addr, mul;
+  const double* p;
+  int mul;
 };
 
 __device__ __forceinline__ double ld_shared_f64(uint32_t a) {
@@ -72,7 +73,7 @@ struct HqlSmem {
 constexpr size_t HQL_V = 0;                                  // V   [32][MAXCAND]
 constexpr size_t HQL_D = HQL_V + (size_t)32 * MAXCAND;
 constexpr size_t HQL_E2 = HQL_D + MAXCAND;
-constexpr size_t HQL_Z = HQL_E2 + MAXCAND;                   // dense Z [MAXCAND][40] (estimator API only)
+constexpr size_t HQL_Z = HQL_E2 + (size_t)MAXCAND * 16;       // dense Z [MAXCAND][40] (estimator API only)
 constexpr size_t HQL_SCRATCH_FUSED = HQL_Z;
 constexpr size_t HQL_SCRATCH_DENSE = HQL_Z + (size_t)MAXCAND * 40;
 
@@ -98,22 +99,22 @@ __device__ __forceinline__ void tree_reduce(double (&acc)[N], double* red) {
 
 // Fused kernel: candidates are window origins cand[j] in the shared support tile.
 struct TileLoader {
-  uint32_t tile_s;       // shared address of tile[0]
+  const double* tile;    // shared
   const uint16_t* cand;  // shared
   __device__ __forceinline__ int base(int j) const { return cand[j]; }
   __device__ __forceinline__ ColRef ref(const HqlSmem& H, int col) const {
     const int off = H.coff[col];
-    return off >= 0 ? ColRef{tile_s + 8u * (uint32_t)off, 8u} : ColRef{smem_addr(&H.cconst[col]), 0u};
+    return off >= 0 ? ColRef{tile + off, 1} : ColRef{&H.cconst[col], 0};
   }
-  __device__ __forceinline__ double at(const ColRef& r, int b) const { return ld_shared_f64(r.addr + (uint32_t)b * r.mul); }
+  __device__ __forceinline__ double at(const ColRef& r, int b) const { return r.p[b * r.mul]; }
 };
 
 // Estimator API: dense Z [m][40] in global memory (all 40 columns stored).
 struct DenseLoader {
   const double* Z;
   __device__ __forceinline__ int base(int j) const { return j * 40; }
-  __device__ __forceinline__ ColRef ref(const HqlSmem&, int col) const { return ColRef{(uint32_t)col, 1u}; }
-  __device__ __forceinline__ double at(const ColRef& r, int b) const { return Z[(size_t)b * r.mul + r.addr]; }
+  __device__ __forceinline__ ColRef ref(const HqlSmem&, int col) const { return ColRef{Z + col, 1}; }
+  __device__ __forceinline__ double at(const ColRef& r, int b) const { return r.p[(size_t)b * r.mul]; }
 };
 
 // Column table of the Z view for target layout n (uoff: tile offsets of the
@@ -161,6 +162,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   const int g = lane >> 2, t4 = lane & 3;
   double* gV = gs + HQL_V;
   double* gD = gs + HQL_D;
+  double* gE2P = gs + HQL_E2;                 // [MAXCAND][8] pairwise accumulators r[g]
+  double* gE2T = gE2P + (size_t)MAXCAND * 8;  // [MAXCAND][8] tail squares
   long long ph_t = clock64();
   const int nks = (m + 3) >> 2;  // k-steps of 4 candidates
   const int nct = (m + 7) >> 3;  // column tiles of 8 candidates
@@ -200,22 +203,50 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     double acc[28];
 #pragma unroll
     for (int i = 0; i < 28; i++) acc[i] = 0.0;
-    // software pipeline: the next k-step's fragments load during this step's MMAs
-    double f[5], fn[5];
-    auto load_f = [&](int s, double(&o)[5]) {
+    // software pipeline: the next k-step's fragments load during this step's
+    // MMAs.  The same raw values also give the candidate's Euclidean distance
+    // to y0 in NumPy's pairwise order (optimize_alpha's nearest set,
+    // estimators.py:222): lane (g,t4) holds dims g, g+8, g+16, g+24 of
+    // candidate 4s+t4 = exactly NumPy's r[g] accumulator; the xor-4/8/16
+    // butterfly is its ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree; the n % 8 tail
+    // dims are added sequentially afterwards.
+    const int n8 = n - (n % 8), ntail = n - n8;
+    double y0g[4];
+#pragma unroll
+    for (int tl = 0; tl < 4; tl++) y0g[tl] = 8 * tl + g < n ? y0[8 * tl + g] : 0.0;
+    double f[5], fn[5], e2p, e2n, tq, tqn;
+    auto load_f = [&](int s, double(&o)[5], double& ep, double& tsq) {
       const int j = 4 * s + t4;
       const bool valid = j < m;
       const int b = zv.base(min(j, m - 1));  // clamped: branch-free loads
+      double r = 0.0;
+      tsq = 0.0;
 #pragma unroll
       for (int tl = 0; tl < 5; tl++) {
-        const double v = zv.at(cr[tl], b) - mu[tl];
-        o[tl] = valid ? v : 0.0;
+        const double raw = zv.at(cr[tl], b);
+        o[tl] = valid ? raw - mu[tl] : 0.0;
+        if (tl < 4) {
+          const double d = raw - y0g[tl];
+          const double sq = __dmul_rn(d, d);
+          if (8 * tl + g < n8) r = __dadd_rn(r, sq);
+          if (8 * tl == n8) tsq = sq;  // tail dim n8 + g (valid if g < ntail)
+        }
+      }
+      ep = r;
+    };
+    // partial sums leave the loop through L2; the tree + tail is done per
+    // candidate by the nearest-set warps (keeps shuffles off the MMA path)
+    auto finish_e2 = [&](int s, double r, double tsq) {
+      const int j = 4 * s + t4;
+      if (j < m) {
+        gE2P[j * 8 + g] = r;
+        gE2T[j * 8 + g] = tsq;
       }
     };
-    load_f(warp, f);
+    load_f(warp, f, e2p, tq);
 #pragma unroll 1
     for (int s = warp; s < nks; s += NWARP) {
-      load_f(s + NWARP, fn);
+      load_f(s + NWARP, fn, e2n, tqn);
       int idx = 0;
 #pragma unroll
       for (int a = 0; a < 4; a++)
@@ -224,8 +255,11 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           dmma(acc[2 * idx], acc[2 * idx + 1], f[a], f[bb]);
           idx++;
         }
+      finish_e2(s, e2p, tq);
 #pragma unroll
       for (int tl = 0; tl < 5; tl++) f[tl] = fn[tl];
+      e2p = e2n;
+      tq = tqn;
     }
     tree_reduce<28>(acc, H.R1);
     double* cyy = H.R1 + R1_SIZE - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
@@ -341,18 +375,20 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       constexpr int NW7 = NT - 32, PER = (MAXCAND + NW7 - 1) / NW7;
       const int t7 = tid - 32, w7 = warp - 1;
       double ev[PER];
+      const int n8 = n - (n % 8), ntail = n - n8;
 #pragma unroll
       for (int i = 0; i < PER; i++) {
         const int j = t7 + i * NW7;
         ev[i] = INFINITY;
-        if (j < m) {
-          const int b = zv.base(j);
-          double v[32];
-#pragma unroll
-          for (int t = 0; t < 32; t++) v[t] = t < n ? zv.at(zv.ref(H, t), b) - y0[t] : 0.0;
-          ev[i] = pairwise_sq32(v, n);
+        if (j < m) {  // NumPy pairwise tree over the covariance pass's partial sums
+          const double* r = gE2P + j * 8;
+          const double* t = gE2T + j * 8;
+          double e = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+          for (int q = 0; q < ntail; q++) e = __dadd_rn(e, t[q]);
+          ev[i] = e;
         }
       }
+      if (tid == 32) atomicAdd(&g_phase_cycles[10], (unsigned long long)(clock64() - ph_t));  // e2 done (diagnostic)
       const int k = min(n + 1, m);
       // (1) per-thread sort of its PER candidates by (e2, index)
       int ej[PER];
@@ -415,6 +451,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           if (lane == 0) H.near[it] = bj;
           if (myj == bj && lane < NWARP - 1) ptr++;
         }
+        if (lane == 0) atomicAdd(&g_phase_cycles[8], (unsigned long long)(clock64() - ph_t));  // nearest side (diagnostic)
       }
     }
     __syncthreads();

@@ -22,3 +22,7 @@ for k, v in ph.items():
         print(f"{k:12s} total {v:.3e} cycles")
     else:
         print(f"{k:12s} {v / max(n_hql,1):10.0f} cycles/HQL patch  {100 * v / tot:5.1f}%")
+kms = _native.kernel_times_ms()[-1]
+busy = ph['patch_idl'] + ph['patch_hql']
+grid = 2 * 148
+print(f"IDL+HQL patch cycles {busy:.3e}; CTA capacity {grid * kms * 1e-3 * 1.965e9:.3e} -> utilisation {busy / (grid * kms * 1e-3 * 1.965e9):.2f}")
