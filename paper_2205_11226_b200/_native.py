@@ -162,10 +162,11 @@ def kernel_times_reset() -> None:
 
 
 PHASES = ["gate", "means", "covariance", "cholesky", "linv", "quadforms", "dmin", "beta", "nearest", "staging",
-          "gram", "loo", "alpha", "chol_only", "patch_idl", "patch_hql"]
+          "e2_done", "loo", "alpha", "chol_only", "patch_idl", "patch_hql",
+          "idl_pick", "idl_gather", "idl_estimate", "idl_writeback"]
 
 
 def phase_cycles(reset: bool = True) -> dict:
-    buf = (ctypes.c_uint64 * 16)()
+    buf = (ctypes.c_uint64 * 24)()
     check(lib().bm_debug_phase_cycles(buf, int(reset)))
     return {name: int(buf[i]) for i, name in enumerate(PHASES)}

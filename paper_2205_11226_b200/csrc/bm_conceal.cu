@@ -63,6 +63,7 @@ struct CellSmem {
   double tile[TILE * TS];
   float tile32[TILE * TS];
   uint64_t lostbits[TILE];
+  uint64_t availbits[TILE];
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
   float rbuf[MAXCAND];   // per expansion-map entry: nu weight, -1 = not admissible
@@ -80,7 +81,8 @@ struct CellSmem {
   int m, m_total, rings_used, max_ring, K, cur_ring;
   double nu, carry, phi;
   unsigned rowmask[6];
-  long long t_start;
+  long long t_start, t_mark, t_pick, t_gather;
+  int idl_diag;
   unsigned long long cnt[8];  // BRL IDL HQL deferred | flop64 flop32 hql gate
   EstSmem est;
   HqlSmem hql;
@@ -269,9 +271,14 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
   }
   __syncthreads();
   if (threadIdx.x < TILE) {
-    uint64_t b = 0;
-    for (int c = 0; c < TILE; c++) b |= (uint64_t)(S.st[threadIdx.x * TS + c] == ST_LO) << c;
+    uint64_t b = 0, a = 0;
+    for (int c = 0; c < TILE; c++) {
+      const uint8_t st = S.st[threadIdx.x * TS + c];
+      b |= (uint64_t)(st == ST_LO) << c;
+      a |= (uint64_t)(st == ST_AV) << c;
+    }
     S.lostbits[threadIdx.x] = b;
+    S.availbits[threadIdx.x] = a;
   }
   __syncthreads();
 }
@@ -428,47 +435,54 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     __syncthreads();
     return;
   }
-  // ---- first chunk, ring by ring
+  // ---- first chunk, ring by ring: per-ring sums in parallel (one warp per
+  // ring), then the reference's sequential nu loop over them
   const int e1 = min(GCH, K);
   screen_chunk(S, g, 0, K, max_ring, R0, C0, true, invf);
-  if (warp == 0) {
+  for (int r = 1 + warp; r <= max_ring && S.ring_off[r] < e1; r += NWARP) {
+    const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
+    double part = 0.0;
+    int c = 0;
+    for (int i = lo + lane; i < hi; i += 32) {
+      const float v = S.rbuf[i];
+      if (v >= 0.f) {
+        part += (double)v;
+        c++;
+      }
+    }
+    part = warp_sum(part);
+    c = warp_sumi(c);
+    if (lane == 0) {
+      S.ringsum[r] = part;
+      S.ringcnt[r] = c;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
     double nu = 0.0, carry = 0.0;
     int cnt_done = 0, stop = 0, r = 1;
     for (; r <= max_ring; r++) {
-      const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
-      double part = 0.0;
-      int c = 0;
-      for (int i = lo + lane; i < hi; i += 32) {
-        const float v = S.rbuf[i];
-        if (v >= 0.f) {
-          part += (double)v;
-          c++;
-        }
-      }
-      part = warp_sum(part);
-      c = warp_sumi(c);
-      cnt_done += c;
+      if (S.ring_off[r] >= e1) break;  // ring starts past the first chunk
+      cnt_done += S.ringcnt[r];
       if (S.ring_off[r + 1] > e1) {  // ring continues past the first chunk
-        carry = part;
+        carry = S.ringsum[r];
         break;
       }
-      nu += part;  // nu += sum of the ring's raw weights (profiles.py:122)
+      nu += S.ringsum[r];  // nu += sum of the ring's raw weights (profiles.py:122)
       if (!(nu < P.t_nu) || r >= max_ring) {
         stop = 1;
         break;
       }
     }
-    if (lane == 0) {
-      S.gated_stop = stop;
-      S.nu = nu;
-      S.carry = carry;
-      S.cur_ring = r;  // stop ring, or the ring straddling the chunk end
-      if (stop) {
-        S.rings_used = r;
-        S.m = cnt_done;
-      }
-      S.pref[0] = cnt_done;  // admissible entries of completed rings
+    S.gated_stop = stop;
+    S.nu = nu;
+    S.carry = carry;
+    S.cur_ring = r;  // stop ring, or the first ring not fully accounted
+    if (stop) {
+      S.rings_used = r;
+      S.m = cnt_done;
     }
+    S.pref[0] = cnt_done;  // admissible entries of the accounted part
   }
   __syncthreads();
   if (S.gated_stop) return;
@@ -558,8 +572,15 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     __syncthreads();
   } else {
     const bool gated = forced < 0;
+    if (tid == 0) S.t_mark = clock64();
     gather(P, S, pr_t, pc_t, gated);
     const int m = S.m;
+    if (tid == 0) {  // diagnostics: pick/extract and gather time of gated IDL-bound patches
+      const long long now = clock64();
+      S.t_pick = S.t_mark - S.t_start;
+      S.t_gather = now - S.t_mark;
+      S.t_mark = now;
+    }
     if (tid == 0 && gated) {
       // nu loop: M_g (3n + 2) FP32 flops; exps counted separately
       S.cnt[5] += (unsigned long long)m * (3 * E.n + 2);
@@ -573,6 +594,13 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     if (gated && !(S.nu < P.t_nu)) {
       // nu >= T_nu -> IDL (profiles.py:123-124); nu > 0 so no underflow
       idl_estimate_dev(acc, m, P.sigma2, E);
+      if (tid == 0) {
+        atomicAdd(&g_phase_cycles[16], (unsigned long long)S.t_pick);
+        atomicAdd(&g_phase_cycles[17], (unsigned long long)S.t_gather);
+        atomicAdd(&g_phase_cycles[18], (unsigned long long)(clock64() - S.t_mark));
+        S.t_mark = clock64();
+        S.idl_diag = 1;
+      }
       if (tid == 0) {
         rec.layer = BM_LAYER_IDL;
         rec.nu = S.nu;
@@ -672,6 +700,10 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     S.lostbits[r] = b;
   }
   if (tid == 0) {
+    if (S.idl_diag) {
+      atomicAdd(&g_phase_cycles[19], (unsigned long long)(clock64() - S.t_mark));
+      S.idl_diag = 0;
+    }
     rec.cycles = (uint32_t)(clock64() - S.t_start);
     if (rec.layer >= BM_LAYER_IDL) atomicAdd(&g_phase_cycles[13 + rec.layer], (unsigned long long)rec.cycles);
     write_record(P, S, rec);
@@ -692,13 +724,17 @@ __device__ void pick_and_extract(CellSmem& S) {
   for (int h = 0; h < 2; h++) {
     const int p = lane + 32 * h;
     if ((pend >> p) & 1ull) {
+      // patch_scores (framework.py:230-240) from the row bitmaps: 6 window rows
+      // of 6 bits, patch cells masked out; out-of-image positions are LOST
       const int pr = patch_r(p), pc = patch_c(p);
       int av = 0, us = 0;
 #pragma unroll
-      for (int k = 0; k < 32; k++) {
-        const uint8_t s = S.st[(pr - 2 + ctx_r(k)) * TS + pc - 2 + ctx_c(k)];
-        av += s == ST_AV;
-        us += s != ST_LO;
+      for (int q = 0; q < 6; q++) {
+        const unsigned m6 = (q == 2 || q == 3) ? 0x33u : 0x3Fu;
+        const unsigned lb = (unsigned)(S.lostbits[pr - 2 + q] >> (pc - 2)) & m6;
+        const unsigned ab = (unsigned)(S.availbits[pr - 2 + q] >> (pc - 2)) & m6;
+        us += __popc(m6 & ~lb);
+        av += __popc(ab);
       }
       const int key = (av << 13) | (us << 7) | (63 - p);
       best_key = max(best_key, key);
@@ -747,6 +783,7 @@ __global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
   const int tid = threadIdx.x;
   double* gS = P.scratch + (size_t)blockIdx.x * P.scratch_per_cta;
   if (tid < 8) S.cnt[tid] = 0;
+  if (tid == 0) S.idl_diag = 0;
   const int nslots = *((volatile int*)P.nslots);
   for (;;) {
     if (tid == 0) S.ticket = atomicAdd(P.ticket, 1u);
@@ -1121,10 +1158,10 @@ extern "C" {
 int bm_abi_version(void) { return BM_ABI_VERSION; }
 
 int bm_debug_phase_cycles(unsigned long long* out16, int reset) {
-  if (cudaMemcpyFromSymbol(out16, g_phase_cycles, 16 * 8) != cudaSuccess) return BM_ERR_CUDA;
+  if (cudaMemcpyFromSymbol(out16, g_phase_cycles, 24 * 8) != cudaSuccess) return BM_ERR_CUDA;
   if (reset) {
-    unsigned long long z[16] = {0};
-    cudaMemcpyToSymbol(g_phase_cycles, z, 16 * 8);
+    unsigned long long z[24] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, 24 * 8);
   }
   return BM_OK;
 }

@@ -143,7 +143,7 @@ __device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
 template <class Acc>
 __device__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S) {
-  const int n = S.n;
+  const int n = S.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double c = 2.0 * sigma2 * n;
   double ex[MAXCAND / NT];
   double emax = -INFINITY;
@@ -155,34 +155,47 @@ __device__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& 
       double v[32];
 #pragma unroll
       for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
-      ex[i] = -pairwise_sq32(v, n) / c;
+      ex[i] = -pairwise_sq32(v, n) / c;  // expo = -d2 / (2 sigma2 N_y)
       emax = fmax(emax, ex[i]);
     }
   }
-  emax = -cta_min(-emax, S);
-  double tot[1] = {0.0};
+  // expo.max(): one barrier
+  emax = warp_max(emax);
+  if (lane == 0) S.redmin[warp] = emax;
+  __syncthreads();
+  emax = S.redmin[0];
 #pragma unroll
-  for (int i = 0; i < MAXCAND / NT; i++) {
-    ex[i] = (threadIdx.x + i * NT < m) ? exp(ex[i] - emax) : 0.0;  // shifted weights
-    tot[0] += ex[i];
-  }
-  cta_sum_n<1>(tot, S);
-  double xs[4] = {0, 0, 0, 0};
+  for (int w = 1; w < NWARP; w++) emax = fmax(emax, S.redmin[w]);
+  // shifted weights and the unnormalised sums in one pass, one barrier
+  double v5[5] = {0, 0, 0, 0, 0};
 #pragma unroll
   for (int i = 0; i < MAXCAND / NT; i++) {
     const int j = threadIdx.x + i * NT;
     if (j < m) {
-      const double w = ex[i] / tot[0];
+      const double sh = exp(ex[i] - emax);
+      v5[0] += sh;
 #pragma unroll
-      for (int q = 0; q < 4; q++) xs[q] = fma(w, acc.x(j, q), xs[q]);
+      for (int q = 0; q < 4; q++) v5[1 + q] = fma(sh, acc.x(j, q), v5[1 + q]);
     }
   }
-  cta_sum_n<4>(xs, S);
+#pragma unroll
+  for (int q = 0; q < 5; q++) v5[q] = warp_sum(v5[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; q++) S.red[warp][q] = v5[q];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
+    double t[5];
+#pragma unroll
+    for (int q = 0; q < 5; q++) {
+      t[q] = S.red[0][q];
+      for (int w = 1; w < NWARP; w++) t[q] += S.red[w][q];
+    }
     const double e0 = exp(emax);  // raw_sum == 0.0 iff the largest term underflows
-    S.nu_raw = e0 * tot[0];
+    S.nu_raw = e0 * t[0];
     S.ok = e0 != 0.0;
-    for (int q = 0; q < 4; q++) S.vals[q] = xs[q];
+    for (int q = 0; q < 4; q++) S.vals[q] = t[1 + q] / t[0];  // w @ x with w = shifted / sum
   }
   __syncthreads();
 }

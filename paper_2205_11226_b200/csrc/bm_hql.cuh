@@ -138,7 +138,7 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
 // (shared, [32]).  Outputs in H/out: ok, vals[4], beta, alpha, gap.
 // Per-phase cycle accounting of the HQL pipeline (thread 0, after barriers);
 // read back with bm_debug_phase_cycles.  Phase 0 = everything before HQL.
-__device__ unsigned long long g_phase_cycles[16];
+__device__ unsigned long long g_phase_cycles[24];
 #define BM_PHASE(k)                                                    \
   do {                                                                 \
     if (threadIdx.x == 0) {                                            \

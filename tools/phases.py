@@ -26,3 +26,6 @@ kms = _native.kernel_times_ms()[-1]
 busy = ph['patch_idl'] + ph['patch_hql']
 grid = 2 * 148
 print(f"IDL+HQL patch cycles {busy:.3e}; CTA capacity {grid * kms * 1e-3 * 1.965e9:.3e} -> utilisation {busy / (grid * kms * 1e-3 * 1.965e9):.2f}")
+nidl = r.summary['layer_counts']['IDL']
+for k in ('idl_pick', 'idl_gather', 'idl_estimate', 'idl_writeback'):
+    print(f"{k:14s} {ph[k] / max(nidl, 1):9.0f} cycles/IDL patch")
