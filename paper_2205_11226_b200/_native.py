@@ -163,7 +163,7 @@ def kernel_times_reset() -> None:
 
 PHASES = ["gate", "means", "covariance", "cholesky", "linv", "quadforms", "dmin", "beta", "nearest", "staging",
           "e2_done", "loo", "alpha", "chol_only", "patch_idl", "patch_hql",
-          "idl_pick", "idl_gather", "idl_estimate", "idl_writeback"]
+          "idl_pick", "idl_gather", "idl_estimate", "idl_writeback", "dep_wait", "patch_brl", "cta_life", "ctas"]
 
 
 def phase_cycles(reset: bool = True) -> dict:

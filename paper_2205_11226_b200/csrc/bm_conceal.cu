@@ -1,5 +1,5 @@
 // bm_conceal.cu — the B200 concealment path: mask preprocessing (lost-cell
-// slots, dependency levels, ticket order), the persistent CTA-per-lost-cell
+// slots, dependency levels, ready FIFOs), the persistent CTA-per-lost-cell
 // concealment kernel, the dense estimator kernel, and the C ABI
 // (include/blockmend_b200.h).
 //
@@ -12,13 +12,17 @@
 //  * one CTA conceals one lost 16x16 cell: it stages the cell's 48x48 support
 //    area (FP64 values, FP32 shadow, states, LOST bitmaps) in shared memory and
 //    runs the cell's whole <=64-patch reliability-ordered chain in place;
-//  * cells are handed out by an atomic ticket in (dependency level, frame,
-//    raster) order; a cell first waits (acquire) for its earlier-raster
-//    8-neighbour lost cells, which reproduces the reference's serial raster
-//    order exactly while independent cells run concurrently;
+//  * dataflow scheduling: a cell becomes ready when its last earlier-raster
+//    lost 8-neighbour finishes (per-cell dependency counters), which
+//    reproduces the reference's serial raster order exactly
+//    while independent cells run concurrently.  Ready cells wait in NB
+//    priority FIFOs keyed by the cell's height in the dependency DAG (longest
+//    chain of dependants first); a CTA pops the highest non-empty FIFO and
+//    never blocks on a dependency;
 //  * a finished cell publishes its 16x16 FP64 values to a per-cell buffer and
-//    releases its flag; later cells read neighbours from those buffers, so the
-//    working image never exists in HBM as a full FP64 copy.
+//    then decrements its dependants' counters; later cells read neighbours
+//    from those buffers, so the working image never exists in HBM as a full
+//    FP64 copy.
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
@@ -47,10 +51,11 @@ struct KParams {
   int* slotmap;        // [B*GR*GC] slot index or -1
   int* slot_cell;      // [ncell] linear cell index of slot
   unsigned* level;     // [ncell]
-  unsigned* order;     // [ncell] slots in ticket order
-  unsigned* done;      // [ncell]
+  unsigned* queue;     // [ncell] ready FIFOs (bucket b at boff[b]); ~0 = not yet written
+  unsigned* indeg;     // [ncell] unfinished earlier-raster lost 8-neighbours
+  unsigned* bucket;    // [ncell] priority bucket of the slot
+  unsigned* sched;     // [SCHED_WORDS]: count[NB], head[NB], tail[NB], boff[NB], claimed
   int* nslots;         // [1]
-  unsigned* ticket;    // [1]
   double* cellbuf;     // [ncell][256]
   uint8_t* rec_count;  // [ncell]
   unsigned long long* counters;  // [12]: BRL, IDL, HQL, deferred, lost_left, bad_states, -, maxlevel,
@@ -73,7 +78,7 @@ struct CellSmem {
   int ringcnt[MAXRING + 2];
   int ring_off[MAXRING + 2];
   // per-patch control (written by warp 0 / thread 0, read after a barrier)
-  int ticket, slot, f, gr, gc;
+  int slot, f, gr, gc;
   unsigned long long remaining, pend;
   int deferred[64];
   int ndef, progressed, nrec;
@@ -151,7 +156,6 @@ __global__ void k_slots(KParams P, const int* flags, const int* excl) {
     if (flags[c]) {
       P.slotmap[c] = excl[c];
       P.slot_cell[excl[c]] = (int)c;
-      P.done[excl[c]] = 0;
     } else {
       P.slotmap[c] = -1;
     }
@@ -226,17 +230,102 @@ __global__ void k_depth(KParams P, unsigned* out) {
   if (!REV && lane == 0) atomicMax((unsigned long long*)&P.counters[7], (unsigned long long)maxlvl);
 }
 
-// Ticket order key: longest chain of dependants first (critical-path
-// priority; a topological order, since a cell's dependants have smaller
-// heights), then level.  Invalid slots (>= nslots) sort last.
-__global__ void k_keys(const unsigned* level, const unsigned* height, const int* nslots, unsigned* key, int n) {
-  const int ns = *nslots;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    key[i] = i < ns ? ((0xFFFFu - min(height[i], 0xFFFEu)) << 16) | min(level[i], 0xFFFFu) : 0xFFFFFFFFu;
+// Dataflow scheduler state.  NB ready FIFOs, bucket 0 = longest chains of
+// dependants (critical-path priority); each FIFO has an exact-size region of
+// the queue array since every slot is pushed exactly once.
+constexpr int NB = 32;
+constexpr int SCHED_COUNT = 0, SCHED_HEAD = 32, SCHED_TAIL = 64, SCHED_BOFF = 96, SCHED_CLAIMED = 128;
+constexpr int SCHED_WORDS = 160;
+
+__device__ __forceinline__ bool cell_lost(const KParams& P, int f, int r, int c, int& slot) {
+  if (r < 0 || r >= P.GR || c < 0 || c >= P.GC) return false;
+  slot = P.slotmap[((size_t)f * P.GR + r) * P.GC + c];
+  return slot >= 0;
 }
 
-__global__ void k_iota(unsigned* v, const int* nslots, int n) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = (unsigned)i;
+// per slot: dependency count (lost earlier-raster 8-neighbours) and priority
+// bucket from the height (longest chain of dependants, k_depth<true>)
+__global__ void k_sched_prep(KParams P, const unsigned* height) {
+  const int ns = *P.nslots;
+  const unsigned maxh = (unsigned)P.counters[7];  // = max level = longest path
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+    const int c = P.slot_cell[s];
+    const int f = c / (P.GR * P.GC), rem = c % (P.GR * P.GC), r = rem / P.GC, cc = rem % P.GC;
+    int d = 0, o;
+    d += cell_lost(P, f, r - 1, cc - 1, o);
+    d += cell_lost(P, f, r - 1, cc, o);
+    d += cell_lost(P, f, r - 1, cc + 1, o);
+    d += cell_lost(P, f, r, cc - 1, o);
+    P.indeg[s] = (unsigned)d;
+    const unsigned h = min(height[s], maxh);
+    const unsigned b = (unsigned)(((unsigned long long)(maxh - h) * NB) / (maxh + 1));
+    P.bucket[s] = b;
+    atomicAdd(&P.sched[SCHED_COUNT + b], 1u);
+  }
+}
+
+// bucket offsets (every block computes them; block 0 publishes) and the
+// initially ready cells (no lost earlier-raster neighbour)
+__global__ void k_sched_seed(KParams P) {
+  __shared__ unsigned boff[NB];
+  if (threadIdx.x == 0) {
+    unsigned o = 0;
+    for (int b = 0; b < NB; b++) {
+      boff[b] = o;
+      o += P.sched[SCHED_COUNT + b];
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < NB) P.sched[SCHED_BOFF + threadIdx.x] = boff[threadIdx.x];
+  const int ns = *P.nslots;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
+    if (P.indeg[s] == 0) {
+      const unsigned b = P.bucket[s];
+      const unsigned t = atomicAdd(&P.sched[SCHED_TAIL + b], 1u);
+      P.queue[boff[b] + t] = (unsigned)s;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned atom_dec_acq_rel(unsigned* p) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(0xFFFFFFFFu) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Pop the next ready cell (warp 0): the highest-priority non-empty FIFO.
+// Returns the slot, or -1 when every cell has been claimed.
+__device__ int sched_pop(const KParams& P, int nslots) {
+  const int lane = threadIdx.x & 31;
+  unsigned* sc = P.sched;
+  for (;;) {
+    const unsigned h = ld_relaxed_u32(&sc[SCHED_HEAD + lane]);
+    const unsigned t = ld_relaxed_u32(&sc[SCHED_TAIL + lane]);
+    const unsigned ne = __ballot_sync(FULL, h < t);
+    if (ne) {
+      const int b = __ffs(ne) - 1;
+      int slot = -2;
+      if (lane == b) {
+        if (atomicCAS(&sc[SCHED_HEAD + b], h, h + 1) == h) {
+          const unsigned* q = P.queue + sc[SCHED_BOFF + b] + h;
+          unsigned v;
+          while ((v = ld_acquire_u32(q)) == 0xFFFFFFFFu) __nanosleep(32);  // reserved, being written
+          slot = (int)v;
+          atomicAdd(&sc[SCHED_CLAIMED], 1u);
+        }
+      }
+      slot = __shfl_sync(FULL, slot, b);
+      if (slot >= 0) return slot;
+      continue;  // lost the race: rescan
+    }
+    if ((int)ld_relaxed_u32(&sc[SCHED_CLAIMED]) >= nslots) return -1;
+    __nanosleep(256);
+  }
 }
 
 // --------------------------------------------------------- the cell kernel
@@ -706,6 +795,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     }
     rec.cycles = (uint32_t)(clock64() - S.t_start);
     if (rec.layer >= BM_LAYER_IDL) atomicAdd(&g_phase_cycles[13 + rec.layer], (unsigned long long)rec.cycles);
+    else atomicAdd(&g_phase_cycles[21], (unsigned long long)rec.cycles);
     write_record(P, S, rec);
     S.nrec++;
     S.cnt[rec.layer]++;
@@ -785,32 +875,25 @@ __global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
   if (tid < 8) S.cnt[tid] = 0;
   if (tid == 0) S.idl_diag = 0;
   const int nslots = *((volatile int*)P.nslots);
+  const long long t_cta0 = clock64();
   for (;;) {
-    if (tid == 0) S.ticket = atomicAdd(P.ticket, 1u);
+    const long long t_w0 = clock64();
+    if (tid < 32) {
+      const int slot = sched_pop(P, nslots);
+      if (tid == 0) S.slot = slot;
+    }
     __syncthreads();
-    const int ticket = S.ticket;
-    if (ticket >= nslots) break;
+    if (S.slot < 0) break;
     if (tid == 0) {
-      const int slot = (int)P.order[ticket];
+      const int slot = S.slot;
       const int c = P.slot_cell[slot];
-      S.slot = slot;
       S.f = c / (P.GR * P.GC);
       const int rem = c % (P.GR * P.GC);
       S.gr = rem / P.GC;
       S.gc = rem % P.GC;
     }
     __syncthreads();
-    // wait for the earlier-raster lost 8-neighbours (profiles.py:298-302 order)
-    if (tid < 4) {
-      const int dr[4] = {-1, -1, -1, 0}, dc[4] = {-1, 0, 1, -1};
-      const int nr = S.gr + dr[tid], nc = S.gc + dc[tid];
-      if (nr >= 0 && nc >= 0 && nc < P.GC) {
-        const int ps = P.slotmap[((size_t)S.f * P.GR + nr) * P.GC + nc];
-        if (ps >= 0)
-          while (ld_acquire_u32(&P.done[ps]) == 0) __nanosleep(64);
-      }
-    }
-    __syncthreads();
+    if (tid == 0) atomicAdd(&g_phase_cycles[20], (unsigned long long)(clock64() - t_w0));  // scheduling wait
     load_tile(P, S);
     // lost_patch_origins (framework.py:219-227)
     if (tid < 32) {
@@ -910,10 +993,25 @@ __global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
       if (tid == 0 && P.records) P.rec_count[slot] = (uint8_t)S.nrec;
       __threadfence();
       __syncthreads();
-      if (tid == 0) st_release_u32(&P.done[slot], 1u);
+      // release the later-raster lost 8-neighbours; the last predecessor of a
+      // cell pushes it to its ready FIFO (acq_rel chain: its data is visible
+      // to whoever pops it)
+      if (tid < 4) {
+        const int dr[4] = {0, 1, 1, 1}, dc[4] = {1, -1, 0, 1};
+        int ps;
+        if (cell_lost(P, f, S.gr + dr[tid], S.gc + dc[tid], ps) && atom_dec_acq_rel(&P.indeg[ps]) == 1u) {
+          const unsigned b = P.bucket[ps];
+          const unsigned t = atomicAdd(&P.sched[SCHED_TAIL + b], 1u);
+          st_release_u32(&P.queue[P.sched[SCHED_BOFF + b] + t], (unsigned)ps);
+        }
+      }
     }
   }
   __syncthreads();
+  if (tid == 0) {
+    atomicAdd(&g_phase_cycles[22], (unsigned long long)(clock64() - t_cta0));  // CTA lifetime
+    atomicAdd(&g_phase_cycles[23], 1ull);
+  }
   if (tid < 4 && S.cnt[tid]) atomicAdd(&P.counters[tid], S.cnt[tid]);
   if (tid >= 4 && tid < 8 && S.cnt[tid]) atomicAdd(&P.counters[tid + 4], S.cnt[tid]);
 }
@@ -1060,8 +1158,8 @@ namespace {
 
 struct Layout {
   size_t ncell;
-  size_t off_slotmap, off_slot_cell, off_level, off_level2, off_height, off_keys, off_order, off_order_in, off_done, off_nslots,
-      off_ticket, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_cub, cub_bytes, off_scratch,
+  size_t off_slotmap, off_slot_cell, off_level, off_level2, off_height, off_bucket, off_queue, off_indeg, off_nslots,
+      off_sched, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_cub, cub_bytes, off_scratch,
       scratch_per_cta, total;
   int grid;
 };
@@ -1111,22 +1209,19 @@ Layout layout(const bm_params* p) {
   L.off_level = o; o = align_up(o + nc * 4);
   L.off_level2 = o; o = align_up(o + nc * 4);
   L.off_height = o; o = align_up(o + nc * 4);
-  L.off_keys = o; o = align_up(o + nc * 4);
-  L.off_order = o; o = align_up(o + nc * 4);
-  L.off_order_in = o; o = align_up(o + nc * 4);
-  L.off_done = o; o = align_up(o + nc * 4);
+  L.off_bucket = o; o = align_up(o + nc * 4);
+  L.off_queue = o; o = align_up(o + nc * 4);
+  L.off_indeg = o; o = align_up(o + nc * 4);
   L.off_nslots = o; o = align_up(o + 4);
-  L.off_ticket = o; o = align_up(o + 4);
+  L.off_sched = o; o = align_up(o + SCHED_WORDS * 4);
   L.off_flags = o; o = align_up(o + nc * 4);
   L.off_excl = o; o = align_up(o + nc * 4);
   L.off_cellbuf = o; o = align_up(o + nc * 256 * 8);
   L.off_reccnt = o; o = align_up(o + nc);
   L.off_counters = o; o = align_up(o + 16 * 8);
-  size_t b1 = 0, b2 = 0;
+  size_t b1 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b1, (int*)nullptr, (int*)nullptr, (int)nc);
-  cub::DeviceRadixSort::SortPairs(nullptr, b2, (unsigned*)nullptr, (unsigned*)nullptr, (unsigned*)nullptr,
-                                  (unsigned*)nullptr, (int)nc);
-  L.cub_bytes = b1 > b2 ? b1 : b2;
+  L.cub_bytes = b1;
   L.off_cub = o; o = align_up(o + L.cub_bytes);
   const int per_sm = cells_per_sm();
   const size_t cap = (size_t)sm_count() * per_sm;
@@ -1236,10 +1331,11 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   P.slotmap = (int*)(ws + L.off_slotmap);
   P.slot_cell = (int*)(ws + L.off_slot_cell);
   P.level = (unsigned*)(ws + L.off_level);
-  P.order = (unsigned*)(ws + L.off_order);
-  P.done = (unsigned*)(ws + L.off_done);
+  P.queue = (unsigned*)(ws + L.off_queue);
+  P.indeg = (unsigned*)(ws + L.off_indeg);
+  P.bucket = (unsigned*)(ws + L.off_bucket);
+  P.sched = (unsigned*)(ws + L.off_sched);
   P.nslots = (int*)(ws + L.off_nslots);
-  P.ticket = (unsigned*)(ws + L.off_ticket);
   P.cellbuf = (double*)(ws + L.off_cellbuf);
   P.rec_count = (uint8_t*)(ws + L.off_reccnt);
   P.counters = (unsigned long long*)(ws + L.off_counters);
@@ -1250,7 +1346,7 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   const int nc = (int)L.ncell;
   cudaError_t e;
   if ((e = cudaMemsetAsync(P.counters, 0, 16 * 8, stream)) != cudaSuccess) return cuda_status(e);
-  if ((e = cudaMemsetAsync(P.ticket, 0, 4, stream)) != cudaSuccess) return cuda_status(e);
+  if ((e = cudaMemsetAsync(P.sched, 0, SCHED_WORDS * 4, stream)) != cudaSuccess) return cuda_status(e);
   if (nc == 0) {
     if ((e = cudaMemsetAsync(P.nslots, 0, 4, stream)) != cudaSuccess) return cuda_status(e);
   }
@@ -1264,17 +1360,12 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
       return cuda_status(e);
     k_slots<<<sms * 4, 256, 0, stream>>>(P, flags, excl);
     unsigned* height = (unsigned*)(ws + L.off_height);
-    unsigned* keys = (unsigned*)(ws + L.off_keys);
     k_depth<false><<<(P.B + 7) / 8, 256, 0, stream>>>(P, P.level);
     k_depth<true><<<(P.B + 7) / 8, 256, 0, stream>>>(P, height);
-    k_keys<<<sms, 256, 0, stream>>>(P.level, height, P.nslots, keys, nc);
-    // ticket order: slots sorted by (height desc, level) (stable -> frame, raster)
-    k_iota<<<sms, 256, 0, stream>>>((unsigned*)(ws + L.off_order_in), P.nslots, nc);
-    cb = L.cub_bytes;
-    if ((e = cub::DeviceRadixSort::SortPairs(ws + L.off_cub, cb, keys, (unsigned*)(ws + L.off_level2),
-                                             (unsigned*)(ws + L.off_order_in), P.order, nc, 0, 32, stream)) !=
-        cudaSuccess)
-      return cuda_status(e);
+    // dataflow scheduler: dependency counters, priority buckets, ready FIFOs
+    if ((e = cudaMemsetAsync(P.queue, 0xFF, (size_t)nc * 4, stream)) != cudaSuccess) return cuda_status(e);
+    k_sched_prep<<<sms, 256, 0, stream>>>(P, height);
+    k_sched_seed<<<sms, 256, 0, stream>>>(P);
     const size_t smem = sizeof(CellSmem);
     if (!g_attr_set) {
       if ((e = cudaFuncSetAttribute(k_conceal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)

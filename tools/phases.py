@@ -29,3 +29,8 @@ print(f"IDL+HQL patch cycles {busy:.3e}; CTA capacity {grid * kms * 1e-3 * 1.965
 nidl = r.summary['layer_counts']['IDL']
 for k in ('idl_pick', 'idl_gather', 'idl_estimate', 'idl_writeback'):
     print(f"{k:14s} {ph[k] / max(nidl, 1):9.0f} cycles/IDL patch")
+cap = ph['cta_life']
+print(f"CTA lifetime {cap:.3e} cycles over {ph['ctas']} CTAs (capacity {grid * kms * 1e-3 * 1.965e9:.3e})")
+for k in ('patch_hql', 'patch_idl', 'patch_brl', 'dep_wait'):
+    print(f"  {k:10s} {100 * ph[k] / cap:5.1f}% of CTA lifetime")
+print(f"  other      {100 * (cap - ph['patch_hql'] - ph['patch_idl'] - ph['patch_brl'] - ph['dep_wait']) / cap:5.1f}%")
