@@ -96,12 +96,16 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    # BM_NATIVE_VARIANT=<tag> loads an in-tree build variant _blockmend_b200.<tag>.so
+    # (tools/ A/B experiments); the default is the product build.
+    tag = os.environ.get("BM_NATIVE_VARIANT")
+    path = LIB_PATH.replace(".so", f".{tag}.so") if tag else LIB_PATH
+    if not os.path.exists(path):
         raise NativeUnavailableError(
-            f"{LIB_PATH} is missing: build it with paper_2205_11226_b200._native.build() "
+            f"{path} is missing: build it with paper_2205_11226_b200._native.build() "
             "(there is no CPU fallback)"
         )
-    L = ctypes.CDLL(LIB_PATH)
+    L = ctypes.CDLL(path)
     vp, i32, i64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
     L.bm_abi_version.restype = ctypes.c_int
     L.bm_status_string.restype = ctypes.c_char_p

@@ -5,8 +5,10 @@
 // K = the candidate count M' (<= 1849):
 //   covariance    C   = Zc^T Zc                 (40 x 40, K = M')   estimators.py:140-142
 //   quadforms     V   = L^-1 (y0 - Y)^T, d = |V_j|^2 (32 x M')       estimators.py:154-158
+//                 (V is consumed in registers; only d leaves the stage)
 //   beta grid     P   = W_beta [Y|X|1]          (24 x 40, K = M')   estimators.py:197-206
-//   alpha Gram    G   = V_near^T V, q = d_i + d_j - 2G (40 x M')     estimators.py:225-229
+//   alpha Gram    G   = U_near (y0 - Y)^T, U = C^-1 (y0 - y_near)    estimators.py:225-229
+//                 (= V_near^T V), q = d_i + d_j - 2G  (40 x M')
 //   LOO sums      Zp  = W_loo [Y|X|1]           (40 x 40, K = M')   estimators.py:231-238
 // Warps own disjoint candidate slices (no barrier inside a pass), keep all
 // output tiles of their slice in registers, and combine them with one
@@ -40,7 +42,10 @@ __device__ __forceinline__ double ld_shared_f64(uint32_t a) {
 }
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
-constexpr int LS = 36;  // stride of Linv / Vn: conflict-free A-fragment loads (36 = 4 mod 16)
+constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (36 = 4 mod 16)
+#ifndef LOO_RR
+#define LOO_RR 1  // 8-row tiles of the nearest set per LOO pass over the candidates
+#endif
 
 constexpr int RED_HALF = NWARP / 2;
 constexpr int ZP_OFF = RED_HALF * 20 * 32;          // Zp rows after the 20-tile partials
@@ -56,7 +61,7 @@ struct HqlSmem {
   double Bm[4 * 32];     // C_XY L^-T
   double cxy[4 * 32];
   double R1[R1_SIZE];    // tree-reduction partials / cyy+L / [ZP_OFF..): Zp rows < 33 / u
-  double R2[1600];       // P (24x40) / Vn (40x36)
+  double R2[1600];       // P (24x40) / Un (40x36)
   double wmin[NWARP][40];
   double rdiag[32];
   double dn[40];
@@ -70,8 +75,7 @@ struct HqlSmem {
 };
 
 // per-CTA global scratch (doubles)
-constexpr size_t HQL_V = 0;                                  // V   [32][MAXCAND]
-constexpr size_t HQL_D = HQL_V + (size_t)32 * MAXCAND;
+constexpr size_t HQL_D = 0;                                  // d_j = |L^-1 (y0 - y_j)|^2
 constexpr size_t HQL_E2 = HQL_D + MAXCAND;
 constexpr size_t HQL_Z = HQL_E2 + (size_t)MAXCAND * 16;       // dense Z [MAXCAND][40] (estimator API only)
 constexpr size_t HQL_SCRATCH_FUSED = HQL_Z;
@@ -102,17 +106,24 @@ struct TileLoader {
   const double* tile;    // shared
   const uint16_t* cand;  // shared
   __device__ __forceinline__ int base(int j) const { return cand[j]; }
-  __device__ __forceinline__ ColRef ref(const HqlSmem& H, int col) const {
+  // shared-space byte address + stride (8, or 0 for a constant column): 2 registers
+  struct Ref {
+    uint32_t a, mul8;
+  };
+  __device__ __forceinline__ Ref ref(const HqlSmem& H, int col) const {
     const int off = H.coff[col];
-    return off >= 0 ? ColRef{tile + off, 1} : ColRef{&H.cconst[col], 0};
+    return off >= 0 ? Ref{smem_addr(tile + off), 8u} : Ref{smem_addr(&H.cconst[col]), 0u};
   }
-  __device__ __forceinline__ double at(const ColRef& r, int b) const { return r.p[b * r.mul]; }
+  __device__ __forceinline__ double at(const Ref& r, int b) const {
+    return *(const double*)__cvta_shared_to_generic((size_t)(r.a + (uint32_t)b * r.mul8));
+  }
 };
 
 // Estimator API: dense Z [m][40] in global memory (all 40 columns stored).
 struct DenseLoader {
   const double* Z;
   __device__ __forceinline__ int base(int j) const { return j * 40; }
+  using Ref = ColRef;
   __device__ __forceinline__ ColRef ref(const HqlSmem&, int col) const { return ColRef{Z + col, 1}; }
   __device__ __forceinline__ double at(const ColRef& r, int b) const { return r.p[(size_t)b * r.mul]; }
 };
@@ -160,7 +171,6 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
                         HqlOut& out) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  double* gV = gs + HQL_V;
   double* gD = gs + HQL_D;
   double* gE2P = gs + HQL_E2;                 // [MAXCAND][8] pairwise accumulators r[g]
   double* gE2T = gE2P + (size_t)MAXCAND * 8;  // [MAXCAND][8] tail squares
@@ -171,7 +181,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   // ---------------------------------------------------------------- means
   {
     double a0 = 0.0, a1 = 0.0;
-    const ColRef c0 = zv.ref(H, lane), c1 = zv.ref(H, lane < 8 ? 32 + lane : 37);
+    const typename ZL::Ref c0 = zv.ref(H, lane), c1 = zv.ref(H, lane < 8 ? 32 + lane : 37);
     for (int j = warp; j < m; j += NWARP) {
       const int b = zv.base(j);
       a0 += zv.at(c0, b);
@@ -192,7 +202,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 
   // ------------------------------------------------- covariance (DMMA)
   {
-    ColRef cr[5];
+    typename ZL::Ref cr[5];
     double mu[5];
 #pragma unroll
     for (int tl = 0; tl < 5; tl++) {
@@ -471,10 +481,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     }
   }
 
-  // ------------------------------------- V = L^-1 (y0 - Y)^T and d (DMMA)
+  // ------------------------------ d_j = |L^-1 (y0 - y_j)|^2 (V in registers, DMMA)
   {
     double y0r[8];
-    ColRef ry[8];
+    typename ZL::Ref ry[8];
 #pragma unroll
     for (int kk = 0; kk < 8; kk++) {
       const int dim = 4 * kk + t4;
@@ -515,8 +525,6 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       for (int r = 0; r < 4; r++) {
         const int row = 8 * r + g;
         const int col = 8 * c + 2 * t4;
-        if (col < m) gV[(size_t)row * MAXCAND + col] = acc[2 * r];
-        if (col + 1 < m) gV[(size_t)row * MAXCAND + col + 1] = acc[2 * r + 1];
         s0 = fma(acc[2 * r], acc[2 * r], s0);
         s1 = fma(acc[2 * r + 1], acc[2 * r + 1], s1);
       }
@@ -548,7 +556,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   }
 
   // ------------------------------------------------ beta grid (DMMA)
-  ColRef crz[5];
+  typename ZL::Ref crz[5];
 #pragma unroll
   for (int ct = 0; ct < 5; ct++) crz[ct] = zv.ref(H, 8 * ct + g);
   {
@@ -642,13 +650,29 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   const double sb = ldexp(1.0, 7 - H.gbest);
   const int k = min(n + 1, m);
 
-  // stage V columns of the nearest set: Vn[i][t] (A fragments of the Gram GEMM)
-  double* Vn = H.R2;  // [40][LS]
-  for (int o = tid; o < 40 * 32; o += NT) {
+  // Rows of the Gram GEMM: U_i = C^-1 (y0 - y_near_i) = L^-T L^-1 (y0 - y_near_i),
+  // so that v_i . v_j = U_i . (y0 - y_j) reads candidate j straight from the
+  // shared support tile (V never goes through global memory).
+  double* Un = H.R2;        // [40][LS]  A fragments of the Gram GEMM
+  double* Vt = H.R1;        // [KMAX][32] L^-1 (y0 - y_near_i) (R1 head is free here)
+  for (int o = tid; o < KMAX * 32; o += NT) {
     const int i = o >> 5, t = o & 31;
-    Vn[i * LS + t] = i < k ? gV[(size_t)t * MAXCAND + H.near[i]] : 0.0;
+    double sv = 0.0;
+    if (i < k && t < n) {
+      const int b = zv.base(H.near[i]);
+      for (int q = 0; q <= t; q++) sv = fma(H.Linv[t * LS + q], y0[q] - zv.at(zv.ref(H, q), b), sv);
+    }
+    Vt[i * 32 + t] = sv;
   }
   if (tid < 40) H.dn[tid] = tid < k ? gD[H.near[tid]] : 0.0;
+  __syncthreads();
+  for (int o = tid; o < 40 * 32; o += NT) {
+    const int i = o >> 5, t = o & 31;
+    double su = 0.0;
+    if (i < k && t < n)
+      for (int q = t; q < n; q++) su = fma(H.Linv[q * LS + t], Vt[i * 32 + q], su);
+    Un[i * LS + t] = su;
+  }
   __syncthreads();
   BM_PHASE(9);
 
@@ -657,68 +681,69 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   // weights exp(x_ij - max_j x_ij), x = -q/(2 beta), are accumulated with a
   // lazily raised per-row reference max (rescale only when a new x exceeds it
   // by > 20, so w <= e^20): identical to the reference's shift after the final
-  // normalisation, and q never round-trips through memory.  One 8-row tile
-  // per pass bounds registers (the V fragments are re-read from L2).
+  // normalisation, and q never round-trips through memory.  LOO_RR 8-row
+  // tiles per pass bound registers; the Gram B fragments (y0 - y_j) are
+  // re-read from the shared support tile each pass.
   double* Zp = H.R1 + ZP_OFF;  // [KMAX][40], after the <=20-tile tree-reduction partials
-  const int npass = (k + 7) >> 3;  // one 8-row tile of the nearest set per pass
-  for (int pass = 0; pass < npass; pass++) {
-    constexpr int RR = 1;  // 8-row tiles per pass
-    const int r0 = pass, nrow = 1;
-    double xref[RR];
-    int nr[RR];
-    double dni[RR];
+  const int ntile = (k + 7) >> 3;  // 8-row tiles of the nearest set
+  constexpr int RR = LOO_RR;       // row tiles per pass over the candidates
+  double y0r[8];
+  typename ZL::Ref ry[8];
 #pragma unroll
-    for (int rr = 0; rr < RR; rr++) {
-      const int i = 8 * (r0 + rr) + g;
-      const bool ok = rr < nrow && i < k;
-      nr[rr] = ok ? H.near[i] : -2;
-      dni[rr] = ok ? H.dn[i] : 0.0;
-      xref[rr] = -INFINITY;
-    }
+  for (int kk = 0; kk < 8; kk++) {
+    const int dim = 4 * kk + t4;
+    y0r[kk] = dim < n ? y0[dim] : 0.0;
+    ry[kk] = zv.ref(H, dim);
+  }
+  for (int r0 = 0; r0 < ntile; r0 += RR) {
+    const int nrow = min(RR, ntile - r0);
+    double xref[RR];
+#pragma unroll
+    for (int rr = 0; rr < RR; rr++) xref[rr] = -INFINITY;
     double acc[10 * RR];
 #pragma unroll
     for (int i = 0; i < 10 * RR; i++) acc[i] = 0.0;
     const int src0 = (g << 2) | (t4 >> 1), src1 = (g << 2) | (2 + (t4 >> 1));
     double fv[8], fvn[8], dv[2], dvn[2];
+    // Gram B fragment of column tile c: (y0 - y_j)[4kk + t4] for j = 8c + g
     auto load_g = [&](int c, double(&o)[8], double(&dd)[2]) {
       const int jB = 8 * c + g;
-      const bool ok = c < nct && jB < m;
+      const bool ok = jB < m;
+      const int bB = zv.base(min(jB, m - 1));
 #pragma unroll
-      for (int kk = 0; kk < 8; kk++) o[kk] = ok ? gV[(size_t)(4 * kk + t4) * MAXCAND + jB] : 0.0;
+      for (int kk = 0; kk < 8; kk++) {
+        const double v = y0r[kk] - zv.at(ry[kk], bB);  // y0r = 0 and column 0 beyond n
+        o[kk] = ok ? v : 0.0;
+      }
       const int col = 8 * c + 2 * t4;
-      dd[0] = (c < nct && col < m) ? gD[col] : 0.0;
-      dd[1] = (c < nct && col + 1 < m) ? gD[col + 1] : 0.0;
+      dd[0] = col < m ? gD[col] : 0.0;
+      dd[1] = col + 1 < m ? gD[col + 1] : 0.0;
     };
     load_g(warp, fv, dv);
 #pragma unroll 1
     for (int c = warp; c < nct; c += NWARP) {
       load_g(c + NWARP, fvn, dvn);
       const int col = 8 * c + 2 * t4;
-      const double d0 = dv[0], d1 = dv[1];
-      double fz[2][5];
-#pragma unroll
-      for (int ks = 0; ks < 2; ks++) {
-        const int j = 8 * c + 4 * ks + t4;
-        const int b = zv.base(min(j, m - 1));  // padding columns get weight 0
-#pragma unroll
-        for (int ct = 0; ct < 5; ct++) fz[ks][ct] = zv.at(crz[ct], b);
-      }
+      const int b0 = zv.base(min(8 * c + t4, m - 1)), b1 = zv.base(min(8 * c + 4 + t4, m - 1));
 #pragma unroll
       for (int rr = 0; rr < RR; rr++) {
         if (rr >= nrow) break;
         const int r = r0 + rr;
+        const int i = 8 * r + g;
+        const int nri = i < k ? H.near[i] : -2;
+        const double dni = i < k ? H.dn[i] : 0.0;
         double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;  // two independent MMA chains
 #pragma unroll
         for (int kk = 0; kk < 8; kk += 2) {
-          dmma(g0, g1, Vn[(8 * r + g) * LS + 4 * kk + t4], fv[kk]);
-          dmma(h0, h1, Vn[(8 * r + g) * LS + 4 * kk + 4 + t4], fv[kk + 1]);
+          dmma(g0, g1, Un[(8 * r + g) * LS + 4 * kk + t4], fv[kk]);
+          dmma(h0, h1, Un[(8 * r + g) * LS + 4 * kk + 4 + t4], fv[kk + 1]);
         }
         g0 += h0;
         g1 += h1;
         double x0 = -INFINITY, x1 = -INFINITY;
-        if (nr[rr] >= 0) {
-          if (col < m && col != nr[rr]) x0 = -(dni[rr] + d0 - 2.0 * g0) * sb;
-          if (col + 1 < m && col + 1 != nr[rr]) x1 = -(dni[rr] + d1 - 2.0 * g1) * sb;
+        if (nri >= 0) {
+          if (col < m && col != nri) x0 = -(dni + dv[0] - 2.0 * g0) * sb;
+          if (col + 1 < m && col + 1 != nri) x1 = -(dni + dv[1] - 2.0 * g1) * sb;
         }
         double tmax = fmax(x0, x1);
         tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 1));
@@ -726,7 +751,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         if (tmax > xref[rr] + 20.0) {  // raise the row's reference, rescale its partial sums
           const double f = xref[rr] == -INFINITY ? 0.0 : exp(xref[rr] - tmax);
 #pragma unroll
-          for (int i = 0; i < 10; i++) acc[rr * 10 + i] *= f;
+          for (int q = 0; q < 10; q++) acc[rr * 10 + q] *= f;
           xref[rr] = tmax;
         }
         const double a0x = x0 - xref[rr], a1x = x1 - xref[rr];
@@ -738,8 +763,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         const double a0 = (t4 & 1) ? s1 : s0, a1 = (t4 & 1) ? u1 : u0;
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
-          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, fz[0][ct]);
-          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a1, fz[1][ct]);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, zv.at(crz[ct], b0));  // padding: weight 0
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a1, zv.at(crz[ct], b1));
         }
       }
 #pragma unroll
@@ -761,16 +786,19 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
       for (int i = 0; i < 10; i++) acc[rr * 10 + i] *= f;
     }
-    tree_reduce<10 * RR>(acc, H.R1);
-    if (warp == 0) {
 #pragma unroll
-      for (int rr = 0; rr < RR; rr++) {
-        const int row = 8 * (r0 + rr) + g;
-        if (rr >= nrow || row >= KMAX) break;
+    for (int rr = 0; rr < RR; rr++) {
+      if (rr >= nrow) break;
+      double a10[10];
+#pragma unroll
+      for (int i = 0; i < 10; i++) a10[i] = acc[rr * 10 + i];
+      tree_reduce<10>(a10, H.R1);
+      const int row = 8 * (r0 + rr) + g;
+      if (warp == 0 && row < KMAX) {
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
-          Zp[row * 40 + 8 * ct + 2 * t4] = acc[rr * 10 + 2 * ct];
-          Zp[row * 40 + 8 * ct + 2 * t4 + 1] = acc[rr * 10 + 2 * ct + 1];
+          Zp[row * 40 + 8 * ct + 2 * t4] = a10[2 * ct];
+          Zp[row * 40 + 8 * ct + 2 * t4 + 1] = a10[2 * ct + 1];
         }
       }
     }
