@@ -86,7 +86,7 @@ struct CellSmem {
   int m, m_total, rings_used, max_ring, K, cur_ring;
   double nu, carry, phi;
   unsigned rowmask[6];
-  long long t_start, t_mark, t_pick, t_gather;
+  long long t_start, t_mark, t_pick, t_gather, t_g[4];
   int idl_diag;
   unsigned long long cnt[8];  // BRL IDL HQL deferred | flop64 flop32 hql gate
   EstSmem est;
@@ -382,7 +382,7 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
 // m_total candidates already gathered.  r is stored per entry in S.rbuf
 // (-1 = not admissible).  Returns the chunk's admissible count (all threads).
 constexpr int GH = 2, GCH = GH * NT;  // entries per chunk: GH per thread
-__device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
+__device__ __noinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
                                             int C0, bool gated, float invf) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
@@ -508,6 +508,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     }
   }
   __syncthreads();
+  if (tid == 0) S.t_g[0] = clock64();
   const int K = S.K, max_ring = S.max_ring;
   if (max_ring == 0) {  // empty expansion map: exhausted before the first ring
     if (tid == 0) { S.m = 0; S.rings_used = 0; }
@@ -528,6 +529,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   // ring), then the reference's sequential nu loop over them
   const int e1 = min(GCH, K);
   screen_chunk(S, g, 0, K, max_ring, R0, C0, true, invf);
+  if (tid == 0) S.t_g[1] = clock64();
   for (int r = 1 + warp; r <= max_ring && S.ring_off[r] < e1; r += NWARP) {
     const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
     double part = 0.0;
@@ -547,6 +549,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     }
   }
   __syncthreads();
+  if (tid == 0) S.t_g[2] = clock64();
   if (tid == 0) {
     double nu = 0.0, carry = 0.0;
     int cnt_done = 0, stop = 0, r = 1;
@@ -574,6 +577,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     S.pref[0] = cnt_done;  // admissible entries of the accounted part
   }
   __syncthreads();
+  if (tid == 0) S.t_g[3] = clock64();
   if (S.gated_stop) return;
   // ---- rest of the map in one sweep, then ring sums and the stopping ring
   for (int e0 = GCH; e0 < K; e0 += GCH) screen_chunk(S, g, e0, K, max_ring, R0, C0, true, invf);
@@ -682,7 +686,17 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     }
     if (gated && !(S.nu < P.t_nu)) {
       // nu >= T_nu -> IDL (profiles.py:123-124); nu > 0 so no underflow
-      idl_estimate_dev(acc, m, P.sigma2, E);
+      idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
+      if (tid == 0 && m < 64) {  // small-m IDL patches: gather / estimate sub-phases
+        atomicAdd(&g_phase_cycles[24], (unsigned long long)(S.t_g[0] - (S.t_mark - S.t_gather)));
+        atomicAdd(&g_phase_cycles[25], (unsigned long long)(S.t_g[1] - S.t_g[0]));
+        atomicAdd(&g_phase_cycles[26], (unsigned long long)(S.t_g[2] - S.t_g[1]));
+        atomicAdd(&g_phase_cycles[27], (unsigned long long)(S.t_g[3] - S.t_g[2]));
+        atomicAdd(&g_phase_cycles[28], (unsigned long long)(E.t_e[0] - S.t_g[3]));
+        atomicAdd(&g_phase_cycles[29], (unsigned long long)(E.t_e[1] - E.t_e[0]));
+        atomicAdd(&g_phase_cycles[30], (unsigned long long)(clock64() - E.t_e[1]));
+        atomicAdd(&g_phase_cycles[31], 1ull);
+      }
       if (tid == 0) {
         atomicAdd(&g_phase_cycles[16], (unsigned long long)S.t_pick);
         atomicAdd(&g_phase_cycles[17], (unsigned long long)S.t_gather);
@@ -699,7 +713,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     } else if (forced == BM_LAYER_IDL) {  // profiles.py:144-153
       bool ok = false;
       if (m >= 1) {
-        idl_estimate_dev(acc, m, P.sigma2, E);
+        idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
         ok = E.ok;
         if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
       }
@@ -742,7 +756,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         }
       }
       if (!done && m >= 1) {
-        idl_estimate_dev(acc, m, P.sigma2, E);
+        idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
         if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
         if (E.ok) {
           done = true;
@@ -1113,7 +1127,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
     }
   }
   if (!done && A.layer != BM_LAYER_BRL && m >= 1) {
-    idl_estimate_dev(acc, m, A.sigma2, E);
+    idl_estimate_dev(acc, m, A.sigma2, E, S.hql.R1);
     rec.nu = E.nu_raw;
     rec.flags |= BM_REC_HAS_NU;
     if (E.ok) {
@@ -1252,11 +1266,11 @@ extern "C" {
 
 int bm_abi_version(void) { return BM_ABI_VERSION; }
 
-int bm_debug_phase_cycles(unsigned long long* out16, int reset) {
-  if (cudaMemcpyFromSymbol(out16, g_phase_cycles, 24 * 8) != cudaSuccess) return BM_ERR_CUDA;
+int bm_debug_phase_cycles(unsigned long long* out32, int reset) {
+  if (cudaMemcpyFromSymbol(out32, g_phase_cycles, 32 * 8) != cudaSuccess) return BM_ERR_CUDA;
   if (reset) {
-    unsigned long long z[24] = {0};
-    cudaMemcpyToSymbol(g_phase_cycles, z, 24 * 8);
+    unsigned long long z[32] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, 32 * 8);
   }
   return BM_OK;
 }

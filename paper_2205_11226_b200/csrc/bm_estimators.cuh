@@ -51,6 +51,7 @@ struct EstSmem {
   double red[NWARP][8];
   double redmin[NWARP];
   float redf[NWARP];
+  long long t_e[2];  // diagnostics
 };
 
 // ----------------------------------------------------------------- helpers
@@ -139,44 +140,40 @@ __device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
 // w = exp(expo - max) / sum, values = w @ x.  (The FP32 Nadaraya-Watson
 // distance/weight work is the nu gate's screening pass in gather(); FP32 in
 // the *estimate* itself is amplified ~1e4x along the patch chain and breaks
-// the +-1 LSB bar.)  Per-candidate values stay in registers.
+// the +-1 LSB bar.)  The exponents go through shared memory
+// (exbuf, >= m doubles).  Not inlined: one copy of the code serves every call
+// site (instruction-cache footprint).
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
 template <class Acc>
-__device__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S) {
+__device__ __noinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf) {
   const int n = S.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double c = 2.0 * sigma2 * n;
-  double ex[MAXCAND / NT];
   double emax = -INFINITY;
+#pragma unroll 1
+  for (int j = threadIdx.x; j < m; j += NT) {
+    double v[32];
 #pragma unroll
-  for (int i = 0; i < MAXCAND / NT; i++) {
-    const int j = threadIdx.x + i * NT;
-    ex[i] = -INFINITY;
-    if (j < m) {
-      double v[32];
-#pragma unroll
-      for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
-      ex[i] = -pairwise_sq32(v, n) / c;  // expo = -d2 / (2 sigma2 N_y)
-      emax = fmax(emax, ex[i]);
-    }
+    for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
+    const double e = -pairwise_sq32(v, n) / c;  // expo = -d2 / (2 sigma2 N_y)
+    exbuf[j] = e;
+    emax = fmax(emax, e);
   }
   // expo.max(): one barrier
   emax = warp_max(emax);
   if (lane == 0) S.redmin[warp] = emax;
   __syncthreads();
+  if (threadIdx.x == 0) S.t_e[0] = clock64();
   emax = S.redmin[0];
 #pragma unroll
   for (int w = 1; w < NWARP; w++) emax = fmax(emax, S.redmin[w]);
   // shifted weights and the unnormalised sums in one pass, one barrier
   double v5[5] = {0, 0, 0, 0, 0};
+#pragma unroll 1
+  for (int j = threadIdx.x; j < m; j += NT) {
+    const double sh = exp(exbuf[j] - emax);
+    v5[0] += sh;
 #pragma unroll
-  for (int i = 0; i < MAXCAND / NT; i++) {
-    const int j = threadIdx.x + i * NT;
-    if (j < m) {
-      const double sh = exp(ex[i] - emax);
-      v5[0] += sh;
-#pragma unroll
-      for (int q = 0; q < 4; q++) v5[1 + q] = fma(sh, acc.x(j, q), v5[1 + q]);
-    }
+    for (int q = 0; q < 4; q++) v5[1 + q] = fma(sh, acc.x(j, q), v5[1 + q]);
   }
 #pragma unroll
   for (int q = 0; q < 5; q++) v5[q] = warp_sum(v5[q]);
@@ -185,6 +182,7 @@ __device__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& 
     for (int q = 0; q < 5; q++) S.red[warp][q] = v5[q];
   }
   __syncthreads();
+  if (threadIdx.x == 0) S.t_e[1] = clock64();
   if (threadIdx.x == 0) {
     double t[5];
 #pragma unroll

@@ -53,6 +53,8 @@ constexpr int R1_SIZE = (RED_HALF * 30 * 32 > ZP_OFF + KMAX * 40 ? RED_HALF * 30
                             ? (RED_HALF * 30 * 32 > ZP_OFF + KMAX * 40 ? RED_HALF * 30 * 32 : ZP_OFF + KMAX * 40)
                             : 2 * 32 * 33;
 
+static_assert(R1_SIZE >= MAXCAND, "HqlSmem::R1 doubles as the IDL exponent buffer");
+
 struct HqlSmem {
   int16_t coff[40];
   double cconst[40];
@@ -149,7 +151,7 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
 // (shared, [32]).  Outputs in H/out: ok, vals[4], beta, alpha, gap.
 // Per-phase cycle accounting of the HQL pipeline (thread 0, after barriers);
 // read back with bm_debug_phase_cycles.  Phase 0 = everything before HQL.
-__device__ unsigned long long g_phase_cycles[24];
+__device__ unsigned long long g_phase_cycles[32];
 #define BM_PHASE(k)                                                    \
   do {                                                                 \
     if (threadIdx.x == 0) {                                            \

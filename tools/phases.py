@@ -34,3 +34,7 @@ print(f"CTA lifetime {cap:.3e} cycles over {ph['ctas']} CTAs (capacity {grid * k
 for k in ('patch_hql', 'patch_idl', 'patch_brl', 'dep_wait'):
     print(f"  {k:10s} {100 * ph[k] / cap:5.1f}% of CTA lifetime")
 print(f"  other      {100 * (cap - ph['patch_hql'] - ph['patch_idl'] - ph['patch_brl'] - ph['dep_wait']) / cap:5.1f}%")
+ns = max(ph['sidl_count'], 1)
+print(f"small-m IDL patches (m < 64): {ph['sidl_count']}")
+for k in ('sidl_setup', 'sidl_screen', 'sidl_ringsums', 'sidl_scan', 'sidl_dist_max', 'sidl_exp_sum', 'sidl_final'):
+    print(f"  {k:14s} {ph[k] / ns:8.0f} cycles")
