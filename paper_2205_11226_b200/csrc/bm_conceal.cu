@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -739,7 +740,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         hql_columns(S.hql, E.n, E.uoff);
         __syncthreads();
         TileLoader zv{S.tile, S.cand};
-        hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout);
+        hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout, E.exptab);
         __syncthreads();
         if (S.hout.ok) {
           done = true;
@@ -887,6 +888,7 @@ __global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
   const int tid = threadIdx.x;
   double* gS = P.scratch + (size_t)blockIdx.x * P.scratch_per_cta;
   if (tid < 8) S.cnt[tid] = 0;
+  init_exptab(S.est);
   if (tid == 0) S.idl_diag = 0;
   const int nslots = *((volatile int*)P.nslots);
   const long long t_cta0 = clock64();
@@ -1089,6 +1091,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
   const double* X = A.x + (size_t)i * A.max_m * 4;
   const double* Y = A.y + (size_t)i * A.max_m * 32;
   double* gs = A.scratch + (size_t)blockIdx.x * HQL_SCRATCH_DENSE;
+  init_exptab(E);
   if (tid < 32) {
     E.y0[tid] = tid < n ? A.y0[(size_t)i * 32 + tid] : 0.0;
     E.y0f[tid] = (float)E.y0[tid];
@@ -1113,7 +1116,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
   bool done = false;
   if (A.layer == BM_LAYER_HQL && m >= 2) {
     DenseLoader zv{Z};
-    hql_mma(zv, m, n, E.y0, S.hql, gs, S.hout);
+    hql_mma(zv, m, n, E.y0, S.hql, gs, S.hout, E.exptab);
     __syncthreads();
     if (S.hout.ok) {
       done = true;
@@ -1202,6 +1205,11 @@ int cells_per_sm() {
         g_attr_set = true;
     }
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_conceal, NT, smem) != cudaSuccess || occ < 1) occ = 1;
+    // dev/diagnostic override (tools/): fewer resident cells per SM
+    if (const char* e = getenv("BM_CELLS_PER_SM")) {
+      const int v = atoi(e);
+      if (v >= 1 && v < occ) occ = v;
+    }
   }
   return occ;
 }

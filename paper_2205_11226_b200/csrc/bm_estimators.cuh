@@ -52,7 +52,12 @@ struct EstSmem {
   double redmin[NWARP];
   float redf[NWARP];
   long long t_e[2];  // diagnostics
+  double exptab[64];  // exp_w table (init_exptab)
 };
+
+__device__ __forceinline__ void init_exptab(EstSmem& S) {
+  if (threadIdx.x < 64) S.exptab[threadIdx.x] = g_exp2_64[threadIdx.x];
+}
 
 // ----------------------------------------------------------------- helpers
 
@@ -170,7 +175,7 @@ __device__ __noinline__ void idl_estimate_dev(const Acc& acc, int m, double sigm
   double v5[5] = {0, 0, 0, 0, 0};
 #pragma unroll 1
   for (int j = threadIdx.x; j < m; j += NT) {
-    const double sh = exp(exbuf[j] - emax);
+    const double sh = exp_w(exbuf[j] - emax, S.exptab);
     v5[0] += sh;
 #pragma unroll
     for (int q = 0; q < 4; q++) v5[1 + q] = fma(sh, acc.x(j, q), v5[1 + q]);

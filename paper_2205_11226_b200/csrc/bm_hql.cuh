@@ -170,7 +170,7 @@ struct HqlOut {
 
 template <class ZL>
 __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H, double* __restrict__ gs,
-                        HqlOut& out) {
+                        HqlOut& out, const double* exptab) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   double* gD = gs + HQL_D;
@@ -587,7 +587,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     for (int s = warp; s < nks; s += NWARP) {
       load_b(s + NWARP, dln, fbn);
       double fa[3];
-      const double e2w = brow ? exp(dl * sc2) : 0.0;  // exp(expo - expo.max())
+      const double e2w = brow ? exp_w(dl * sc2, exptab) : 0.0;  // exp(expo - expo.max())
       fa[2] = e2w;
       fa[1] = e2w * e2w;
       fa[0] = fa[1] * fa[1];
@@ -757,8 +757,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           xref[rr] = tmax;
         }
         const double a0x = x0 - xref[rr], a1x = x1 - xref[rr];
-        const double w0 = a0x > -746.0 ? exp(a0x) : 0.0;  // exp underflows to 0 below
-        const double w1 = a1x > -746.0 ? exp(a1x) : 0.0;
+        const double w0 = exp_w(a0x, exptab), w1 = exp_w(a1x, exptab);
         // C-fragment layout (row g, cols 2t4..2t4+1) -> A fragments of the two k-steps
         const double s0 = __shfl_sync(FULL, w0, src0), s1 = __shfl_sync(FULL, w1, src0);
         const double u0 = __shfl_sync(FULL, w0, src1), u1 = __shfl_sync(FULL, w1, src1);
