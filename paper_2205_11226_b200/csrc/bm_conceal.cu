@@ -72,7 +72,10 @@ struct CellSmem {
   uint64_t availbits[TILE];
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
-  float rbuf[MAXCAND];   // per expansion-map entry: nu weight, -1 = not admissible
+  union {
+    float rbuf[MAXCAND];   // gate: per expansion-map entry nu weight, -1 = not admissible
+    double dbuf[MAXCAND];  // HQL: d_j = |L^-1 (y0 - y_j)|^2
+  };
   int pref[2];
   int wcnt[2 * NWARP];
   double ringsum[MAXRING + 2];
@@ -740,7 +743,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         hql_columns(S.hql, E.n, E.uoff);
         __syncthreads();
         TileLoader zv{S.tile, S.cand};
-        hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout, E.exptab);
+        hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout, E.exptab, S.dbuf);
         __syncthreads();
         if (S.hout.ok) {
           done = true;
@@ -1077,6 +1080,7 @@ struct EstBatchArgs {
 };
 
 struct EstBatchSmem {
+  double dbuf[MAXCAND];
   EstSmem est;
   HqlSmem hql;
   HqlOut hout;
@@ -1116,7 +1120,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
   bool done = false;
   if (A.layer == BM_LAYER_HQL && m >= 2) {
     DenseLoader zv{Z};
-    hql_mma(zv, m, n, E.y0, S.hql, gs, S.hout, E.exptab);
+    hql_mma(zv, m, n, E.y0, S.hql, gs, S.hout, E.exptab, S.dbuf);
     __syncthreads();
     if (S.hout.ok) {
       done = true;

@@ -48,10 +48,10 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #endif
 
 constexpr int RED_HALF = NWARP / 2;
-constexpr int ZP_OFF = RED_HALF * 20 * 32;          // Zp rows after the 20-tile partials
-constexpr int R1_SIZE = (RED_HALF * 30 * 32 > ZP_OFF + KMAX * 40 ? RED_HALF * 30 * 32 : ZP_OFF + KMAX * 40) > 2 * 32 * 33
-                            ? (RED_HALF * 30 * 32 > ZP_OFF + KMAX * 40 ? RED_HALF * 30 * 32 : ZP_OFF + KMAX * 40)
-                            : 2 * 32 * 33;
+constexpr int RED_CHUNK = 15;                         // tree reductions in chunks of <= 15 values
+constexpr int ZP_OFF = RED_HALF * 10 * 32;             // Zp rows after the LOO's 10-value partials
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int R1_SIZE = cmax(cmax(ZP_OFF + KMAX * 40, 2 * 32 * 33), cmax(RED_HALF * RED_CHUNK * 32, MAXCAND));
 
 static_assert(R1_SIZE >= MAXCAND, "HqlSmem::R1 doubles as the IDL exponent buffer");
 
@@ -77,28 +77,32 @@ struct HqlSmem {
 };
 
 // per-CTA global scratch (doubles)
-constexpr size_t HQL_D = 0;                                  // d_j = |L^-1 (y0 - y_j)|^2
-constexpr size_t HQL_E2 = HQL_D + MAXCAND;
+constexpr size_t HQL_E2 = 0;
 constexpr size_t HQL_Z = HQL_E2 + (size_t)MAXCAND * 16;       // dense Z [MAXCAND][40] (estimator API only)
 constexpr size_t HQL_SCRATCH_FUSED = HQL_Z;
 constexpr size_t HQL_SCRATCH_DENSE = HQL_Z + (size_t)MAXCAND * 40;
 
-// Fixed-order tree reduction of per-warp register tiles (NWARP warps -> warp 0);
-// red must hold (NWARP/2) * N * 32 doubles.
-template <int N>
+// Fixed-order tree reduction of per-warp register tiles (NWARP warps -> warp 0)
+// in chunks of C values; red must hold (NWARP/2) * C * 32 doubles.
+template <int N, int C = N>
 __device__ __forceinline__ void tree_reduce(double (&acc)[N], double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int half = NWARP / 2; half >= 1; half >>= 1) {
-    __syncthreads();
-    if (warp >= half && warp < 2 * half) {
+  for (int c0 = 0; c0 < N; c0 += C) {
 #pragma unroll
-      for (int i = 0; i < N; i++) red[((warp - half) * N + i) * 32 + lane] = acc[i];
-    }
-    __syncthreads();
-    if (warp < half) {
+    for (int half = NWARP / 2; half >= 1; half >>= 1) {
+      __syncthreads();
+      if (warp >= half && warp < 2 * half) {
 #pragma unroll
-      for (int i = 0; i < N; i++) acc[i] += red[(warp * N + i) * 32 + lane];
+        for (int i = 0; i < C; i++)
+          if (c0 + i < N) red[((warp - half) * C + i) * 32 + lane] = acc[c0 + i];
+      }
+      __syncthreads();
+      if (warp < half) {
+#pragma unroll
+        for (int i = 0; i < C; i++)
+          if (c0 + i < N) acc[c0 + i] += red[(warp * C + i) * 32 + lane];
+      }
     }
   }
 }
@@ -170,10 +174,9 @@ struct HqlOut {
 
 template <class ZL>
 __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H, double* __restrict__ gs,
-                        HqlOut& out, const double* exptab) {
+                        HqlOut& out, const double* exptab, double* dS) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  double* gD = gs + HQL_D;
   double* gE2P = gs + HQL_E2;                 // [MAXCAND][8] pairwise accumulators r[g]
   double* gE2T = gE2P + (size_t)MAXCAND * 8;  // [MAXCAND][8] tail squares
   long long ph_t = clock64();
@@ -273,7 +276,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       e2p = e2n;
       tq = tqn;
     }
-    tree_reduce<28>(acc, H.R1);
+    tree_reduce<28, 14>(acc, H.R1);
     double* cyy = H.R1 + R1_SIZE - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
     double* L = cyy + 32 * 33;
     __syncwarp();
@@ -537,8 +540,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
       if (g == 0) {
         const int col = 8 * c + 2 * t4;
-        if (col < m) gD[col] = s0;
-        if (col + 1 < m) gD[col + 1] = s1;
+        if (col < m) dS[col] = s0;
+        if (col + 1 < m) dS[col + 1] = s1;
       }
     }
   }
@@ -547,7 +550,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   double dmin;
   {
     double mn = INFINITY;
-    for (int j = tid; j < m; j += NT) mn = fmin(mn, gD[j]);
+    for (int j = tid; j < m; j += NT) mn = fmin(mn, dS[j]);
     mn = warp_min(mn);
     if (lane == 0) H.redmin[0][warp] = mn;
     __syncthreads();
@@ -577,7 +580,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       const bool valid = j < m;
       const int jc = min(j, m - 1);
       const int b = zv.base(jc);
-      const double dd = dmin - gD[jc];
+      const double dd = dmin - dS[jc];
       d = valid ? dd : -INFINITY;  // -inf -> weight 0 for padding
 #pragma unroll
       for (int ct = 0; ct < 5; ct++) o[ct] = zv.at(crz[ct], b);  // weight 0 for padding
@@ -599,7 +602,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
       for (int ct = 0; ct < 5; ct++) fb[ct] = fbn[ct];
     }
-    tree_reduce<30>(acc, H.R1);
+    tree_reduce<30, RED_CHUNK>(acc, H.R1);
     double* P = H.R2;  // [24][40]
     if (warp == 0) {
 #pragma unroll
@@ -666,7 +669,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     }
     Vt[i * 32 + t] = sv;
   }
-  if (tid < 40) H.dn[tid] = tid < k ? gD[H.near[tid]] : 0.0;
+  if (tid < 40) H.dn[tid] = tid < k ? dS[H.near[tid]] : 0.0;
   __syncthreads();
   for (int o = tid; o < 40 * 32; o += NT) {
     const int i = o >> 5, t = o & 31;
@@ -705,28 +708,23 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     double acc[10 * RR];
 #pragma unroll
     for (int i = 0; i < 10 * RR; i++) acc[i] = 0.0;
-    const int src0 = (g << 2) | (t4 >> 1), src1 = (g << 2) | (2 + (t4 >> 1));
-    double fv[8], fvn[8], dv[2], dvn[2];
+    double fv[8], fvn[8];
     // Gram B fragment of column tile c: (y0 - y_j)[4kk + t4] for j = 8c + g
-    auto load_g = [&](int c, double(&o)[8], double(&dd)[2]) {
-      const int jB = 8 * c + g;
-      const bool ok = jB < m;
-      const int bB = zv.base(min(jB, m - 1));
+    auto load_g = [&](int c, double(&o)[8]) {
+      const int bB = zv.base(min(8 * c + g, m - 1));  // padding columns: clamped (their x is -inf)
 #pragma unroll
-      for (int kk = 0; kk < 8; kk++) {
-        const double v = y0r[kk] - zv.at(ry[kk], bB);  // y0r = 0 and column 0 beyond n
-        o[kk] = ok ? v : 0.0;
-      }
-      const int col = 8 * c + 2 * t4;
-      dd[0] = col < m ? gD[col] : 0.0;
-      dd[1] = col + 1 < m ? gD[col + 1] : 0.0;
+      for (int kk = 0; kk < 8; kk++) o[kk] = y0r[kk] - zv.at(ry[kk], bB);  // y0r = 0 and column 0 beyond n
     };
-    load_g(warp, fv, dv);
+    load_g(warp, fv);
 #pragma unroll 1
     for (int c = warp; c < nct; c += NWARP) {
-      load_g(c + NWARP, fvn, dvn);
+      load_g(c + NWARP, fvn);
       const int col = 8 * c + 2 * t4;
-      const int b0 = zv.base(min(8 * c + t4, m - 1)), b1 = zv.base(min(8 * c + 4 + t4, m - 1));
+      const double dv0 = dS[min(col, m - 1)], dv1 = dS[min(col + 1, m - 1)];
+      // k-step 0 takes the tile's even candidates 8c + 2t4, k-step 1 the odd
+      // ones: the Gram C fragment (row g, cols 2t4, 2t4+1) is then already the
+      // A fragment of both k-steps, no shuffles
+      const int b0 = zv.base(min(col, m - 1)), b1 = zv.base(min(col + 1, m - 1));
 #pragma unroll
       for (int rr = 0; rr < RR; rr++) {
         if (rr >= nrow) break;
@@ -744,24 +742,23 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         g1 += h1;
         double x0 = -INFINITY, x1 = -INFINITY;
         if (nri >= 0) {
-          if (col < m && col != nri) x0 = -(dni + dv[0] - 2.0 * g0) * sb;
-          if (col + 1 < m && col + 1 != nri) x1 = -(dni + dv[1] - 2.0 * g1) * sb;
+          if (col < m && col != nri) x0 = -(dni + dv0 - 2.0 * g0) * sb;
+          if (col + 1 < m && col + 1 != nri) x1 = -(dni + dv1 - 2.0 * g1) * sb;
         }
-        double tmax = fmax(x0, x1);
-        tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 1));
-        tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 2));
-        if (tmax > xref[rr] + 20.0) {  // raise the row's reference, rescale its partial sums
-          const double f = xref[rr] == -INFINITY ? 0.0 : exp(xref[rr] - tmax);
+        if (__any_sync(FULL, fmax(x0, x1) > xref[rr] + 20.0)) {
+          // (rare) raise the row references, rescale the rows' partial sums
+          double tmax = fmax(x0, x1);
+          tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 1));
+          tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 2));
+          if (tmax > xref[rr] + 20.0) {
+            const double f = xref[rr] == -INFINITY ? 0.0 : exp(xref[rr] - tmax);
 #pragma unroll
-          for (int q = 0; q < 10; q++) acc[rr * 10 + q] *= f;
-          xref[rr] = tmax;
+            for (int q = 0; q < 10; q++) acc[rr * 10 + q] *= f;
+            xref[rr] = tmax;
+          }
         }
-        const double a0x = x0 - xref[rr], a1x = x1 - xref[rr];
-        const double w0 = exp_w(a0x, exptab), w1 = exp_w(a1x, exptab);
-        // C-fragment layout (row g, cols 2t4..2t4+1) -> A fragments of the two k-steps
-        const double s0 = __shfl_sync(FULL, w0, src0), s1 = __shfl_sync(FULL, w1, src0);
-        const double u0 = __shfl_sync(FULL, w0, src1), u1 = __shfl_sync(FULL, w1, src1);
-        const double a0 = (t4 & 1) ? s1 : s0, a1 = (t4 & 1) ? u1 : u0;
+        const double a0 = x0 == -INFINITY ? 0.0 : exp_w(x0 - xref[rr], exptab);
+        const double a1 = x1 == -INFINITY ? 0.0 : exp_w(x1 - xref[rr], exptab);
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
           dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, zv.at(crz[ct], b0));  // padding: weight 0
@@ -770,8 +767,6 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
 #pragma unroll
       for (int kk = 0; kk < 8; kk++) fv[kk] = fvn[kk];
-      dv[0] = dvn[0];
-      dv[1] = dvn[1];
     }
     // combine the warps' partial sums at a common per-row reference
 #pragma unroll
