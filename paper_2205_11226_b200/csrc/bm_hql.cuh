@@ -27,13 +27,9 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-// Candidate loaders.  Column col of candidate j: columns 0..31 = y (N_y used,
-// rest 0), 32..35 = x, 36 = 1 (sums), 37..39 = 0.  A lane resolves its
-// columns once into ColRefs; a fragment element is then one IMAD + one load.
-struct ColRef {
-  const double* p;
-  int mul;
-};
+// Candidate loaders.  Column col of candidate j: columns 0..31 = y (N_y used),
+// 32..35 = x, 36 = 1 (sums), 37..39 unused.  A lane resolves its columns once
+// into Refs; a fragment element is then one IMAD + one load.
 
 __device__ __forceinline__ double ld_shared_f64(uint32_t a) {
   double v;
@@ -57,7 +53,6 @@ static_assert(R1_SIZE >= MAXCAND, "HqlSmem::R1 doubles as the IDL exponent buffe
 
 struct HqlSmem {
   int16_t coff[40];
-  double cconst[40];
   double mean[40];
   double Linv[32 * LS];
   double Bm[4 * 32];     // C_XY L^-T
@@ -112,26 +107,29 @@ struct TileLoader {
   const double* tile;    // shared
   const uint16_t* cand;  // shared
   __device__ __forceinline__ int base(int j) const { return cand[j]; }
-  // shared-space byte address + stride (8, or 0 for a constant column): 2 registers
-  struct Ref {
-    uint32_t a, mul8;
-  };
+  // shared-space byte address of the column at window origin 0 (1 register).
+  // Constant columns (y beyond n, the ones column 36, 37..39) alias a real
+  // tile column: every consumer either ignores those outputs, multiplies
+  // them by exact zeros (U / L^-1 vanish beyond n), or substitutes the ones
+  // column itself (ONES_COL).
+  using Ref = uint32_t;
   __device__ __forceinline__ Ref ref(const HqlSmem& H, int col) const {
     const int off = H.coff[col];
-    return off >= 0 ? Ref{smem_addr(tile + off), 8u} : Ref{smem_addr(&H.cconst[col]), 0u};
+    return smem_addr(tile + (off >= 0 ? off : 0));
   }
-  __device__ __forceinline__ double at(const Ref& r, int b) const {
-    return *(const double*)__cvta_shared_to_generic((size_t)(r.a + (uint32_t)b * r.mul8));
+  __device__ __forceinline__ double at(Ref r, int b) const {
+    return *(const double*)__cvta_shared_to_generic((size_t)(r + (uint32_t)b * 8u));
   }
 };
+constexpr int ONES_COL = 36;  // Z column of ones: its weighted sum is the weight total
 
 // Estimator API: dense Z [m][40] in global memory (all 40 columns stored).
 struct DenseLoader {
   const double* Z;
   __device__ __forceinline__ int base(int j) const { return j * 40; }
-  using Ref = ColRef;
-  __device__ __forceinline__ ColRef ref(const HqlSmem&, int col) const { return ColRef{Z + col, 1}; }
-  __device__ __forceinline__ double at(const ColRef& r, int b) const { return r.p[(size_t)b * r.mul]; }
+  using Ref = const double*;
+  __device__ __forceinline__ Ref ref(const HqlSmem&, int col) const { return Z + col; }
+  __device__ __forceinline__ double at(Ref r, int b) const { return r[b]; }
 };
 
 // Column table of the Z view for target layout n (uoff: tile offsets of the
@@ -140,14 +138,12 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
   const int t = threadIdx.x;
   if (t < 40) {
     int16_t off = -1;
-    double c = 0.0;
     if (t < n) off = uoff ? uoff[t] : (int16_t)t;
     else if (t >= 32 && t < 36) {
       const int q = t - 32;
       off = uoff ? (int16_t)((2 + (q >> 1)) * TS + 2 + (q & 1)) : (int16_t)t;
-    } else if (t == 36) c = 1.0;
+    }
     H.coff[t] = off;
-    H.cconst[t] = c;
   }
 }
 
@@ -383,7 +379,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         x[i] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);
       }
 #pragma unroll
-      for (int i = 0; i < 32; i++) H.Linv[i * LS + lane] = x[i];
+      for (int i = 0; i < 32; i++) H.Linv[i * LS + lane] = (i < n && lane < n) ? x[i] : 0.0;  // zero beyond n
     } else {
       // warps 1..7: Euclidean distances in NumPy's order and the stable
       // k-nearest selection (optimize_alpha, estimators.py:221-223)
@@ -584,6 +580,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       d = valid ? dd : -INFINITY;  // -inf -> weight 0 for padding
 #pragma unroll
       for (int ct = 0; ct < 5; ct++) o[ct] = zv.at(crz[ct], b);  // weight 0 for padding
+      if (g == ONES_COL - 32) o[4] = 1.0;
     };
     load_b(warp, dl, fb);
 #pragma unroll 1
@@ -725,6 +722,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // ones: the Gram C fragment (row g, cols 2t4, 2t4+1) is then already the
       // A fragment of both k-steps, no shuffles
       const int b0 = zv.base(min(col, m - 1)), b1 = zv.base(min(col + 1, m - 1));
+      const bool ones = g == ONES_COL - 32;
 #pragma unroll
       for (int rr = 0; rr < RR; rr++) {
         if (rr >= nrow) break;
@@ -761,8 +759,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         const double a1 = x1 == -INFINITY ? 0.0 : exp_w(x1 - xref[rr], exptab);
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
-          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, zv.at(crz[ct], b0));  // padding: weight 0
-          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a1, zv.at(crz[ct], b1));
+          const double z0 = ct == 4 && ones ? 1.0 : zv.at(crz[ct], b0);  // padding: weight 0
+          const double z1 = ct == 4 && ones ? 1.0 : zv.at(crz[ct], b1);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, z0);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a1, z1);
         }
       }
 #pragma unroll
