@@ -117,9 +117,9 @@ int64_t bm_max_records(const bm_params* p);
  * launch; up to 256 kept).  Synchronises on the events.  Returns the count. */
 int bm_kernel_times_ms(float* out, int cap);
 void bm_kernel_times_reset(void);
-/* Diagnostics: 32 cumulative SM-cycle counters (HQL phases, IDL patch
+/* Diagnostics: 40 cumulative SM-cycle counters (HQL phases, IDL patch
  * phases, scheduling); names in _native.PHASES. */
-int bm_debug_phase_cycles(unsigned long long* out32, int reset);
+int bm_debug_phase_cycles(unsigned long long* out40, int reset);
 /* SM clock of the current device in kHz (converts bm_patch_record.cycles to
  * seconds for ConcealmentReport.patch_times); 0 when no device. */
 int bm_device_clock_khz(void);

@@ -168,10 +168,11 @@ def kernel_times_reset() -> None:
 PHASES = ["gate", "means", "covariance", "cholesky", "linv", "quadforms", "dmin", "beta", "nearest", "staging",
           "e2_done", "loo", "alpha", "chol_only", "patch_idl", "patch_hql",
           "idl_pick", "idl_gather", "idl_estimate", "idl_writeback", "dep_wait", "patch_brl", "cta_life", "ctas",
-          "sidl_setup", "sidl_screen", "sidl_ringsums", "sidl_scan", "sidl_dist_max", "sidl_exp_sum", "sidl_final", "sidl_count"]
+          "sidl_setup", "sidl_screen", "sidl_ringsums", "sidl_scan", "sidl_dist_max", "sidl_exp_sum", "sidl_final", "sidl_count",
+          "beta_loop_t0", "beta_loop_reduce", "loo_loops_t0", "x35", "x36", "x37", "x38", "x39"]
 
 
 def phase_cycles(reset: bool = True) -> dict:
-    buf = (ctypes.c_uint64 * 32)()
+    buf = (ctypes.c_uint64 * 40)()
     check(lib().bm_debug_phase_cycles(buf, int(reset)))
     return {name: int(buf[i]) for i, name in enumerate(PHASES)}

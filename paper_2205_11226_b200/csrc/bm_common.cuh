@@ -224,21 +224,32 @@ __device__ const double g_exp2_64[64] = {  // copied to shared memory per CTA (E
     0x1.d5818dcfba487p+0, 0x1.da9e603db3285p+0, 0x1.dfc97337b9b5fp+0, 0x1.e502ee78b3ff6p+0,
     0x1.ea4afa2a490dap+0, 0x1.efa1bee615a27p+0, 0x1.f50765b6e4540p+0, 0x1.fa7c1819e90d8p+0,
 };
-__device__ __forceinline__ double exp_w(double a, const double* __restrict__ tab) {
-  const double ac = fmax(a, -708.0);
-  const double t = fma(ac, 0x1.71547652b82fep+6, 0x1.8p52);  // round(a * 64 / ln2) in the low word
+// coefficients in the constant bank (direct DFMA operands, no register moves)
+__device__ __constant__ double c_expw[6] = {
+    0x1.71547652b82fep+6,                        // 64 / ln2
+    0x1.62e4200000000p-7, 0x1.fdf473de6af28p-28,  // ln2 / 64 = hi + lo (hi * k exact for |k| < 2^20)
+    0x1.5555555555555p-3, 0x1.1111111111111p-7, 0x1.5555555555555p-5};  // 1/6, 1/120, 1/24
+// a <= 709 and a not NaN (the weight arguments in the beta grid and LOO,
+// <= 20 by construction); a < -708 -> 0
+__device__ __forceinline__ double exp_wn(double a, const double* __restrict__ tab) {
+  const double ac = a < -708.0 ? -708.0 : a;
+  const double t = fma(ac, c_expw[0], 0x1.8p52);  // round(a * 64 / ln2) in the low word
   const int ki = __double2loint(t);
   const double kd = t - 0x1.8p52;
-  double r = fma(kd, -0x1.62e4200000000p-7, ac);
-  r = fma(kd, -0x1.fdf473de6af28p-28, r);
+  double r = fma(kd, -c_expw[1], ac);
+  r = fma(kd, -c_expw[2], r);
   const double r2 = r * r;
   const double p01 = r + 1.0;
-  const double p23 = fma(r, 0x1.5555555555555p-3, 0.5);
-  const double p45 = fma(r, 0x1.1111111111111p-7, 0x1.5555555555555p-5);
-  const double p = fma(r2, fma(r2, p45, p23), p01);
-  const double s = tab[ki & 63] * __hiloint2double((((ki >> 6) + 1023) << 20), 0);
-  const double res = a >= -708.0 ? p * s : 0.0;
-  return a <= 709.0 ? res : a * INFINITY;  // NaN stays NaN, overflow -> inf
+  const double p23 = fma(r, c_expw[3], 0.5);
+  const double p45 = fma(r, c_expw[4], c_expw[5]);
+  const double v = fma(r2, fma(r2, p45, p23), p01) * tab[ki & 63];  // in [0.99, 2)
+  const double res = __hiloint2double(__double2hiint(v) + ((ki >> 6) << 20), __double2loint(v));  // * 2^(ki>>6)
+  return a >= -708.0 ? res : 0.0;
+}
+// general version: NaN stays NaN, overflow -> inf
+__device__ __forceinline__ double exp_w(double a, const double* __restrict__ tab) {
+  const double res = exp_wn(a, tab);
+  return a <= 709.0 ? res : a * INFINITY;
 }
 
 }  // namespace bm

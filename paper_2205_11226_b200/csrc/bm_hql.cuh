@@ -167,7 +167,7 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
 // (shared, [32]).  Outputs in H/out: ok, vals[4], beta, alpha, gap.
 // Per-phase cycle accounting of the HQL pipeline (thread 0, after barriers);
 // read back with bm_debug_phase_cycles.  Phase 0 = everything before HQL.
-__device__ unsigned long long g_phase_cycles[32];
+__device__ unsigned long long g_phase_cycles[40];
 #define BM_PHASE(k)                                                    \
   do {                                                                 \
     if (threadIdx.x == 0) {                                            \
@@ -611,7 +611,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     for (int s = warp; s < nks; s += NWARP) {
       load_b(s + NWARP, dln, fbn);
       double fa[3];
-      const double e2w = brow ? exp_w(dl * sc2, exptab) : 0.0;  // exp(expo - expo.max())
+      const double e2w = brow ? exp_wn(dl * sc2, exptab) : 0.0;  // exp(expo - expo.max()); -inf -> 0
       fa[2] = e2w;
       fa[1] = e2w * e2w;
       fa[0] = fa[1] * fa[1];
@@ -625,7 +625,9 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       for (int ct = 0; ct < 5; ct++) fb[ct] = fbn[ct];
     }
     });
+    if (tid == 0) atomicAdd(&g_phase_cycles[32], (unsigned long long)(clock64() - ph_t));  // beta loop (thread 0)
     tree_reduce<30, RED_CHUNK>(acc, H.R1);
+    if (tid == 0) atomicAdd(&g_phase_cycles[33], (unsigned long long)(clock64() - ph_t));  // beta loop + reduce
     double* P = H.R2;  // [24][40]
     if (warp == 0) {
 #pragma unroll
@@ -724,6 +726,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     ry[kk] = zv.ref(H, dim);
   }
   for (int r0 = 0; r0 < ntile; r0 += RR) {
+    const long long t_pass = clock64();
     const int nrow = min(RR, ntile - r0);
     double xref[RR];
 #pragma unroll
@@ -782,8 +785,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
             xref[rr] = tmax;
           }
         }
-        const double a0 = x0 == -INFINITY ? 0.0 : exp_w(x0 - xref[rr], exptab);
-        const double a1 = x1 == -INFINITY ? 0.0 : exp_w(x1 - xref[rr], exptab);
+        const double e0 = exp_wn(x0 - xref[rr], exptab), e1 = exp_wn(x1 - xref[rr], exptab);
+        const double a0 = x0 == -INFINITY ? 0.0 : e0, a1 = x1 == -INFINITY ? 0.0 : e1;  // (xref may be -inf)
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
           if (ct >= NA && ct < 4) continue;  // y columns beyond n: outputs unused
@@ -795,6 +798,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
     }
     });
+    if (tid == 0) atomicAdd(&g_phase_cycles[34], (unsigned long long)(clock64() - t_pass));  // LOO loops (thread 0)
     // combine the warps' partial sums at a common per-row reference
 #pragma unroll
     for (int rr = 0; rr < RR; rr++)

@@ -38,3 +38,5 @@ ns = max(ph['sidl_count'], 1)
 print(f"small-m IDL patches (m < 64): {ph['sidl_count']}")
 for k in ('sidl_setup', 'sidl_screen', 'sidl_ringsums', 'sidl_scan', 'sidl_dist_max', 'sidl_exp_sum', 'sidl_final'):
     print(f"  {k:14s} {ph[k] / ns:8.0f} cycles")
+print(f"beta: loop(t0) {ph['beta_loop_t0'] / max(n_hql,1):.0f}  loop+reduce {ph['beta_loop_reduce'] / max(n_hql,1):.0f}  (phase total {ph['beta'] / max(n_hql,1):.0f})")
+print(f"loo: loops(t0) {ph['loo_loops_t0'] / max(n_hql,1):.0f}  (phase total {ph['loo'] / max(n_hql,1):.0f})")
