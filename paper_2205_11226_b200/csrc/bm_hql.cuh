@@ -628,7 +628,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     if (tid == 0) atomicAdd(&g_phase_cycles[32], (unsigned long long)(clock64() - ph_t));  // beta loop (thread 0)
     tree_reduce<30, RED_CHUNK>(acc, H.R1);
     if (tid == 0) atomicAdd(&g_phase_cycles[33], (unsigned long long)(clock64() - ph_t));  // beta loop + reduce
-    double* P = H.R2;  // [24][40]
+    constexpr int PS = 41;  // row stride of P: conflict-free per-lane row reads
+    double* P = H.R2;       // [24][PS]
     if (warp == 0) {
 #pragma unroll
       for (int r = 0; r < 3; r++)
@@ -636,38 +637,44 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         for (int ct = 0; ct < 5; ct++) {
           const int bi = 3 * g + r;  // grid index of MMA row 8r+g
           if (bi < 24) {
-            P[bi * 40 + 8 * ct + 2 * t4] = acc[2 * (r * 5 + ct)];
-            P[bi * 40 + 8 * ct + 2 * t4 + 1] = acc[2 * (r * 5 + ct) + 1];
+            P[bi * PS + 8 * ct + 2 * t4] = acc[2 * (r * 5 + ct)];
+            P[bi * PS + 8 * ct + 2 * t4 + 1] = acc[2 * (r * 5 + ct) + 1];
           }
         }
       __syncwarp();
       // eps_g = ||y0 - y~0(beta_g)||^2 in NumPy's pairwise order; strict < argmin
       double eps = INFINITY;
       if (lane < NBETA) {
-        const double S = P[lane * 40 + 36];
+        const double invS = 1.0 / P[lane * PS + ONES_COL];
         eps = pairwise_sum_n(n, [&](int t) {
-          const double d = y0[t] - P[lane * 40 + t] / S;
+          const double d = y0[t] - P[lane * PS + t] * invS;
           return __dmul_rn(d, d);
         });
       }
-      double best_eps = INFINITY;
-      int best = 0;
-      for (int gg = 0; gg < NBETA; gg++) {
-        const double e = __shfl_sync(FULL, eps, gg);
-        if (e < best_eps) { best_eps = e; best = gg; }
+      // first minimum (ties -> smaller beta; NaN never wins), butterfly over (key, index)
+      double bv = eps != eps ? INFINITY : eps;
+      int bi = lane;
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(FULL, bv, o);
+        const int oi = __shfl_xor_sync(FULL, bi, o);
+        if (ov < bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
       }
+      const int best = bv == INFINITY ? 0 : bi;
+      const double best_eps = __shfl_sync(FULL, eps, best) != __shfl_sync(FULL, eps, best) ? INFINITY
+                                                                                          : __shfl_sync(FULL, eps, best);
       double ya = lane < n ? fabs(y0[lane]) : 0.0;
       ya = warp_max(ya);
       const double dy = 1e-11 * ya;
       const double noise = 2.0 * sqrt(best_eps * n) * dy + n * dy * dy + 1e-300;
-      double gap = INFINITY;
-      for (int gg = 0; gg < NBETA; gg++) {
-        const double e = __shfl_sync(FULL, eps, gg);
-        if (gg != best) gap = fmin(gap, fabs(e - best_eps) / noise);
-      }
-      const double S = P[best * 40 + 36];
-      H.yt[lane] = lane < n ? P[best * 40 + lane] / S : 0.0;
-      if (lane < 4) H.xt[lane] = P[best * 40 + 32 + lane] / S;
+      double gap = (lane < NBETA && lane != best) ? fabs(eps - best_eps) / noise : INFINITY;
+      gap = warp_min(gap);
+      const double invS = 1.0 / P[best * PS + ONES_COL];
+      H.yt[lane] = lane < n ? P[best * PS + lane] * invS : 0.0;
+      if (lane < 4) H.xt[lane] = P[best * PS + 32 + lane] * invS;
       if (lane == 0) {
         H.gbest = best;
         out.beta = ldexp(1.0, best - 8);
