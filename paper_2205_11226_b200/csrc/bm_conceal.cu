@@ -386,7 +386,7 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
 // m_total candidates already gathered.  r is stored per entry in S.rbuf
 // (-1 = not admissible).  Returns the chunk's admissible count (all threads).
 constexpr int GH = 2, GCH = GH * NT;  // entries per chunk: GH per thread
-__device__ __noinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
+__device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
                                             int C0, bool gated, float invf) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
@@ -520,8 +520,67 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     return;
   }
   const float invf = (float)(1.0 / (2.0 * P.sigma2 * n));
+  // one screening loop (a single inlined copy of screen_chunk): ungated = the
+  // whole map; gated = the first chunk, its ring-by-ring nu stop, then the
+  // rest of the map in one sweep
+  const int e1 = min(GCH, K);
+  for (int e0 = 0; e0 < K; e0 += GCH) {
+    screen_chunk(S, g, e0, K, max_ring, R0, C0, gated, invf);
+    if (!gated || e0 > 0) continue;
+    if (tid == 0) S.t_g[1] = clock64();
+    // ---- first chunk, ring by ring: per-ring sums in parallel (one warp per
+    // ring), then the reference's sequential nu loop over them
+    for (int r = 1 + warp; r <= max_ring && S.ring_off[r] < e1; r += NWARP) {
+      const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
+      double part = 0.0;
+      int c = 0;
+      for (int i = lo + lane; i < hi; i += 32) {
+        const float v = S.rbuf[i];
+        if (v >= 0.f) {
+          part += (double)v;
+          c++;
+        }
+      }
+      part = warp_sum(part);
+      c = warp_sumi(c);
+      if (lane == 0) {
+        S.ringsum[r] = part;
+        S.ringcnt[r] = c;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) S.t_g[2] = clock64();
+    if (tid == 0) {
+      double nu = 0.0, carry = 0.0;
+      int cnt_done = 0, stop = 0, r = 1;
+      for (; r <= max_ring; r++) {
+        if (S.ring_off[r] >= e1) break;  // ring starts past the first chunk
+        cnt_done += S.ringcnt[r];
+        if (S.ring_off[r + 1] > e1) {  // ring continues past the first chunk
+          carry = S.ringsum[r];
+          break;
+        }
+        nu += S.ringsum[r];  // nu += sum of the ring's raw weights (profiles.py:122)
+        if (!(nu < P.t_nu) || r >= max_ring) {
+          stop = 1;
+          break;
+        }
+      }
+      S.gated_stop = stop;
+      S.nu = nu;
+      S.carry = carry;
+      S.cur_ring = r;  // stop ring, or the first ring not fully accounted
+      if (stop) {
+        S.rings_used = r;
+        S.m = cnt_done;
+      }
+      S.pref[0] = cnt_done;  // admissible entries of the accounted part
+    }
+    __syncthreads();
+    if (tid == 0) S.t_g[3] = clock64();
+    if (S.gated_stop) return;
+  }
   if (!gated) {
-    for (int e0 = 0; e0 < K; e0 += GCH) screen_chunk(S, g, e0, K, max_ring, R0, C0, false, invf);
     if (tid == 0) {
       S.m = S.m_total;
       S.rings_used = max_ring;
@@ -529,62 +588,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     __syncthreads();
     return;
   }
-  // ---- first chunk, ring by ring: per-ring sums in parallel (one warp per
-  // ring), then the reference's sequential nu loop over them
-  const int e1 = min(GCH, K);
-  screen_chunk(S, g, 0, K, max_ring, R0, C0, true, invf);
-  if (tid == 0) S.t_g[1] = clock64();
-  for (int r = 1 + warp; r <= max_ring && S.ring_off[r] < e1; r += NWARP) {
-    const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
-    double part = 0.0;
-    int c = 0;
-    for (int i = lo + lane; i < hi; i += 32) {
-      const float v = S.rbuf[i];
-      if (v >= 0.f) {
-        part += (double)v;
-        c++;
-      }
-    }
-    part = warp_sum(part);
-    c = warp_sumi(c);
-    if (lane == 0) {
-      S.ringsum[r] = part;
-      S.ringcnt[r] = c;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) S.t_g[2] = clock64();
-  if (tid == 0) {
-    double nu = 0.0, carry = 0.0;
-    int cnt_done = 0, stop = 0, r = 1;
-    for (; r <= max_ring; r++) {
-      if (S.ring_off[r] >= e1) break;  // ring starts past the first chunk
-      cnt_done += S.ringcnt[r];
-      if (S.ring_off[r + 1] > e1) {  // ring continues past the first chunk
-        carry = S.ringsum[r];
-        break;
-      }
-      nu += S.ringsum[r];  // nu += sum of the ring's raw weights (profiles.py:122)
-      if (!(nu < P.t_nu) || r >= max_ring) {
-        stop = 1;
-        break;
-      }
-    }
-    S.gated_stop = stop;
-    S.nu = nu;
-    S.carry = carry;
-    S.cur_ring = r;  // stop ring, or the first ring not fully accounted
-    if (stop) {
-      S.rings_used = r;
-      S.m = cnt_done;
-    }
-    S.pref[0] = cnt_done;  // admissible entries of the accounted part
-  }
-  __syncthreads();
-  if (tid == 0) S.t_g[3] = clock64();
-  if (S.gated_stop) return;
-  // ---- rest of the map in one sweep, then ring sums and the stopping ring
-  for (int e0 = GCH; e0 < K; e0 += GCH) screen_chunk(S, g, e0, K, max_ring, R0, C0, true, invf);
+  // ---- the rest of the map was screened in the same loop: ring sums and the stopping ring
   const int rs = S.cur_ring;  // first ring not yet accounted (may have a carry)
   for (int r = rs + warp; r <= max_ring; r += NWARP) {
     const int lo = max(S.ring_off[r], r == rs ? e1 : 0), hi = S.ring_off[r + 1];
@@ -688,9 +692,38 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
       rec.rings_used = (uint8_t)S.rings_used;
       rec.m_candidates = m;
     }
-    if (gated && !(S.nu < P.t_nu)) {
-      // nu >= T_nu -> IDL (profiles.py:123-124); nu > 0 so no underflow
+    // layer ladder with one IDL call site: 0 = gated IDL (nu >= T_nu,
+    // profiles.py:123-124), 1 = forced IDL (profiles.py:144-153), 2 = HQL
+    // with its ladder HQL -> IDL -> BRL (estimators.py:248-286)
+    const int mode = (gated && !(S.nu < P.t_nu)) ? 0 : (forced == BM_LAYER_IDL ? 1 : 2);
+    bool done = false;
+    if (mode == 2 && m >= 2) {
+      if (tid == 0) atomicAdd(&g_phase_cycles[0], (unsigned long long)(clock64() - S.t_start));
+      hql_columns(S.hql, E.n, E.uoff);
+      __syncthreads();
+      TileLoader zv{S.tile, S.cand};
+      hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout, E.exptab, S.dbuf);
+      __syncthreads();
+      if (S.hout.ok) {
+        done = true;
+        if (tid == 0) {
+          for (int q = 0; q < 4; q++) E.vals[q] = S.hout.vals[q];
+          S.cnt[4] += hql_flops(m, E.n);
+          S.cnt[6]++;
+          rec.layer = BM_LAYER_HQL;
+          rec.beta = S.hout.beta;
+          rec.alpha = S.hout.alpha;
+          rec.beta_gap = S.hout.gap;
+          rec.flags |= BM_REC_HAS_BW;
+        }
+      }
+    }
+    const bool run_idl = !done && m >= 1;  // (mode 0 has m >= 1: nu > 0)
+    if (run_idl) {
       idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
+      if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
+    }
+    if (mode == 0) {
       if (tid == 0 && m < 64) {  // small-m IDL patches: gather / estimate sub-phases
         atomicAdd(&g_phase_cycles[24], (unsigned long long)(S.t_g[0] - (S.t_mark - S.t_gather)));
         atomicAdd(&g_phase_cycles[25], (unsigned long long)(S.t_g[1] - S.t_g[0]));
@@ -707,21 +740,12 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         atomicAdd(&g_phase_cycles[18], (unsigned long long)(clock64() - S.t_mark));
         S.t_mark = clock64();
         S.idl_diag = 1;
-      }
-      if (tid == 0) {
         rec.layer = BM_LAYER_IDL;
         rec.nu = S.nu;
         rec.flags |= BM_REC_HAS_NU;
-        S.cnt[4] += idl_flops(m, E.n);
       }
-    } else if (forced == BM_LAYER_IDL) {  // profiles.py:144-153
-      bool ok = false;
-      if (m >= 1) {
-        idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
-        ok = E.ok;
-        if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
-      }
-      if (ok) {
+    } else if (mode == 1) {
+      if (run_idl && E.ok) {
         if (tid == 0) {
           rec.layer = BM_LAYER_IDL;
           rec.nu = E.nu_raw;
@@ -736,41 +760,14 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
         }
       }
     } else {
-      // HQL with its ladder (estimators.py:248-286)
-      bool done = false;
-      if (m >= 2) {
-        if (tid == 0) atomicAdd(&g_phase_cycles[0], (unsigned long long)(clock64() - S.t_start));
-        hql_columns(S.hql, E.n, E.uoff);
-        __syncthreads();
-        TileLoader zv{S.tile, S.cand};
-        hql_mma(zv, m, E.n, E.y0, S.hql, gS, S.hout, E.exptab, S.dbuf);
-        __syncthreads();
-        if (S.hout.ok) {
-          done = true;
-          if (tid == 0) {
-            for (int q = 0; q < 4; q++) E.vals[q] = S.hout.vals[q];
-            S.cnt[4] += hql_flops(m, E.n);
-            S.cnt[6]++;
-            rec.layer = BM_LAYER_HQL;
-            rec.beta = S.hout.beta;
-            rec.alpha = S.hout.alpha;
-            rec.beta_gap = S.hout.gap;
-            rec.flags |= BM_REC_HAS_BW;
-          }
-        }
-      }
-      if (!done && m >= 1) {
-        idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
-        if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
-        if (E.ok) {
-          done = true;
-          if (tid == 0) {
-            rec.layer = BM_LAYER_IDL;
-            rec.flags |= BM_REC_FALLBACK;
-            if (!gated) {
-              rec.nu = E.nu_raw;
-              rec.flags |= BM_REC_HAS_NU;
-            }
+      if (run_idl && E.ok) {
+        done = true;
+        if (tid == 0) {
+          rec.layer = BM_LAYER_IDL;
+          rec.flags |= BM_REC_FALLBACK;
+          if (!gated) {
+            rec.nu = E.nu_raw;
+            rec.flags |= BM_REC_HAS_NU;
           }
         }
       }

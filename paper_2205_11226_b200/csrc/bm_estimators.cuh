@@ -146,11 +146,11 @@ __device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
 // distance/weight work is the nu gate's screening pass in gather(); FP32 in
 // the *estimate* itself is amplified ~1e4x along the patch chain and breaks
 // the +-1 LSB bar.)  The exponents go through shared memory
-// (exbuf, >= m doubles).  Not inlined: one copy of the code serves every call
-// site (instruction-cache footprint).
+// (exbuf, >= m doubles).  Called from one site per kernel (one inlined copy:
+// instruction-cache footprint).
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
 template <class Acc>
-__device__ __noinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf) {
+__device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf) {
   const int n = S.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double c = 2.0 * sigma2 * n;
   double emax = -INFINITY;
