@@ -720,7 +720,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     }
     const bool run_idl = !done && m >= 1;  // (mode 0 has m >= 1: nu > 0)
     if (run_idl) {
-      idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1);
+      idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1, mode != 0);
       if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
     }
     if (mode == 0) {
@@ -1131,7 +1131,7 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
     }
   }
   if (!done && A.layer != BM_LAYER_BRL && m >= 1) {
-    idl_estimate_dev(acc, m, A.sigma2, E, S.hql.R1);
+    idl_estimate_dev(acc, m, A.sigma2, E, S.hql.R1, true);
     rec.nu = E.nu_raw;
     rec.flags |= BM_REC_HAS_NU;
     if (E.ok) {

@@ -150,7 +150,8 @@ __device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
 // instruction-cache footprint).
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
 template <class Acc>
-__device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf) {
+__device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf,
+                                                 bool want_raw) {
   const int n = S.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double c = 2.0 * sigma2 * n;
   double emax = -INFINITY;
@@ -188,17 +189,25 @@ __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double s
   }
   __syncthreads();
   if (threadIdx.x == 0) S.t_e[1] = clock64();
-  if (threadIdx.x == 0) {
-    double t[5];
+  if (warp == 0) {
+    // lane q < 5 totals sum q over the warps (fixed order)
+    double t = 0.0;
+    if (lane < 5) {
+      t = S.red[0][lane];
 #pragma unroll
-    for (int q = 0; q < 5; q++) {
-      t[q] = S.red[0][q];
-      for (int w = 1; w < NWARP; w++) t[q] += S.red[w][q];
+      for (int w = 1; w < NWARP; w++) t += S.red[w][lane];
     }
-    const double e0 = exp(emax);  // raw_sum == 0.0 iff the largest term underflows
-    S.nu_raw = e0 * t[0];
-    S.ok = e0 != 0.0;
-    for (int q = 0; q < 4; q++) S.vals[q] = t[1 + q] / t[0];  // w @ x with w = shifted / sum
+    const double t0 = __shfl_sync(FULL, t, 0);
+    if (lane >= 1 && lane < 5) S.vals[lane - 1] = t * (1.0 / t0);  // w @ x with w = shifted / sum
+    if (lane == 0) {
+      if (want_raw) {  // forced / fallback IDL: raw_sum and the underflow test
+        const double e0 = exp(emax);  // raw_sum == 0.0 iff the largest term underflows
+        S.nu_raw = e0 * t0;
+        S.ok = e0 != 0.0;
+      } else {
+        S.ok = 1;  // gated IDL: nu >= T_nu > 0, no underflow
+      }
+    }
   }
   __syncthreads();
 }
