@@ -52,11 +52,11 @@ struct EstSmem {
   double redmin[NWARP];
   float redf[NWARP];
   long long t_e[2];  // diagnostics
-  double exptab[64];  // exp_w table (init_exptab)
+  alignas(16) double exptab[128];  // exp_w table (init_exptab)
 };
 
 __device__ __forceinline__ void init_exptab(EstSmem& S) {
-  if (threadIdx.x < 64) S.exptab[threadIdx.x] = g_exp2_64[threadIdx.x];
+  if (threadIdx.x < 128) S.exptab[threadIdx.x] = g_exp2_64[threadIdx.x];
 }
 
 // ----------------------------------------------------------------- helpers

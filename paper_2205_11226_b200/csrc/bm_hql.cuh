@@ -645,9 +645,9 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // eps_g = ||y0 - y~0(beta_g)||^2 in NumPy's pairwise order; strict < argmin
       double eps = INFINITY;
       if (lane < NBETA) {
-        const double invS = 1.0 / P[lane * PS + ONES_COL];
+        const double S = P[lane * PS + ONES_COL];
         eps = pairwise_sum_n(n, [&](int t) {
-          const double d = y0[t] - P[lane * PS + t] * invS;
+          const double d = y0[t] - P[lane * PS + t] / S;
           return __dmul_rn(d, d);
         });
       }
@@ -672,9 +672,9 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       const double noise = 2.0 * sqrt(best_eps * n) * dy + n * dy * dy + 1e-300;
       double gap = (lane < NBETA && lane != best) ? fabs(eps - best_eps) / noise : INFINITY;
       gap = warp_min(gap);
-      const double invS = 1.0 / P[best * PS + ONES_COL];
-      H.yt[lane] = lane < n ? P[best * PS + lane] * invS : 0.0;
-      if (lane < 4) H.xt[lane] = P[best * PS + 32 + lane] * invS;
+      const double S = P[best * PS + ONES_COL];
+      H.yt[lane] = lane < n ? P[best * PS + lane] / S : 0.0;
+      if (lane < 4) H.xt[lane] = P[best * PS + 32 + lane] / S;
       if (lane == 0) {
         H.gbest = best;
         out.beta = ldexp(1.0, best - 8);

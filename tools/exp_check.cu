@@ -3,8 +3,8 @@
 #include <cmath>
 #include "../paper_2205_11226_b200/csrc/bm_common.cuh"
 __global__ void k(double* maxulp, unsigned long long* cnt, double lo, double hi, long n) {
-  __shared__ double tab[64];
-  if (threadIdx.x < 64) tab[threadIdx.x] = bm::g_exp2_64[threadIdx.x];
+  __shared__ __align__(16) double tab[128];
+  if (threadIdx.x < 128) tab[threadIdx.x] = bm::g_exp2_64[threadIdx.x];
   __syncthreads();
   double mu = 0;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
@@ -17,8 +17,8 @@ __global__ void k(double* maxulp, unsigned long long* cnt, double lo, double hi,
   atomicMax((unsigned long long*)maxulp, __double_as_longlong(mu));
 }
 __global__ void k_special(double* out) {
-  __shared__ double tab[64];
-  if (threadIdx.x < 64) tab[threadIdx.x] = bm::g_exp2_64[threadIdx.x];
+  __shared__ __align__(16) double tab[128];
+  if (threadIdx.x < 128) tab[threadIdx.x] = bm::g_exp2_64[threadIdx.x];
   __syncthreads();
   if (threadIdx.x == 0) {
     out[0] = bm::exp_w(-INFINITY, tab);
@@ -35,7 +35,7 @@ int main() {
   double mu; unsigned long long nz;
   cudaMemcpy(&mu, d, 8, cudaMemcpyDeviceToHost); cudaMemcpy(&nz, c, 8, cudaMemcpyDeviceToHost);
   printf("exp_w max error %.3f ulp over 2e8 points in [-708, 25]; nonzero below -708: %llu\n", mu, nz);
-  k_special<<<1, 64>>>(d);
+  k_special<<<1, 128>>>(d);
   double s[5]; cudaMemcpy(s, d, 40, cudaMemcpyDeviceToHost);
   printf("exp_w(-inf)=%g exp_w(nan)=%g exp_w(1000)=%g exp_w(0)=%.17g exp_w(-708)=%g (exp %g)\n", s[0], s[1], s[2], s[3], s[4], exp(-708.0));
   return 0;
