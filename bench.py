@@ -33,8 +33,14 @@ from paper_2205_11226_b200.synth import CONFIGS, make_config  # noqa: E402
 
 METRIC = "lost 16x16 blocks concealed/sec"
 UNIT = "blocks/s"
-FP64_PEAK_TFLOPS = 36.2  # measured DFMA peak on this pool's B200 (tools/peakbench.cu, profiles/peaks_r01.txt)
+# FP64 peak: DMMA (mma.sync m8n8k4 f64) and DFMA share the SM's FP64 hardware
+# (tools/pipebench.cu: mixing them does not add up); the measured ceiling is
+# 36.8 TF/s DMMA, 36.2 DFMA (profiles/peaks_r01.txt) -> the roofline uses 36.8.
+FP64_PEAK_TFLOPS = 36.8
 FP32_PEAK_TFLOPS = 69.7  # measured FFMA peak (same run)
+LAUNCHES_PER_STEP = 11   # k_init_out, k_cell_flags, 2 x CUB scan, k_slots, 2 x k_depth,
+                         # k_sched_prep, k_sched_seed, k_conceal, k_summary (profiles/ launch list)
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")  # ncu --set full dram bytes per launch
 
 WORKLOADS = {
     # name: (cfg, profile, forced_layer)
@@ -42,6 +48,7 @@ WORKLOADS = {
     "cfg2": (2, "efficient", None),
     "cfg3": (3, "efficient", None),
     "cfg4": (4, "sentinel", "HQL"),
+    "cfg4idl": (4, "sentinel", "IDL"),  # forced IDL: the distance/weight-stage stress
     "cfg5": (5, "efficient", None),
 }
 
@@ -175,6 +182,8 @@ def cpu_baseline(workload: str, jobs=None):
     cells = sum(r[0] for r in res)
     return {
         "value": cells / wall,
+        "cells": int(cells),
+        "wall_s": wall,
         "unit": UNIT,
         "cores": cores,
         "kind": "port",
@@ -188,13 +197,16 @@ def run_reference(args, rank, world):
         return
     jobs = cpu_jobs(args.workload)
     times = []
+    cells = []
     last = None
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         last = cpu_baseline(args.workload, jobs)
         if i >= args.warmup:
             times.append(time.perf_counter() - t0)
-    value = last["value"]
+            cells.append(last["cells"])
+    value = float(np.sum(cells)) / float(np.sum(times))  # lost cells over the timed steps / their wall time
+    last = dict(last, value=value)
     cfg, prof_name, forced = WORKLOADS[args.workload]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
@@ -336,13 +348,27 @@ def main():
         if kmean:
             a64 = flop64 / (kmean * 1e-3) / 1e12
             a32 = flop32 / (kmean * 1e-3) / 1e12
+            traffic = None
+            try:
+                with open(TRAFFIC_FILE) as fh:
+                    tr = json.load(fh).get(args.workload)
+                if tr and tr.get("frames") == int(px.shape[0]):  # same launch size as profiled
+                    traffic = tr["dram_bytes_per_launch"]
+            except (OSError, ValueError):
+                pass
             roof = {
                 "bound": "fp64", "achieved": a64, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": a64 / FP64_PEAK_TFLOPS, "traffic": None,
+                "frac": a64 / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "traffic_unit": "bytes per k_conceal launch (dram__bytes_read.sum + dram__bytes_write.sum, "
+                                "ncu --set full, profiles/ncu_traffic.json)",
+                "algorithmic_bytes_per_launch": int(px.numel() * 2 + out_u8.numel()),
                 "kernel": "bm::k_conceal", "kernel_ms": kmean, "kernel_share_of_step": kmean / ms_per_step,
                 "flop64_per_launch": flop64, "flop32_per_launch": flop32,
                 "fp32_gate": {"achieved": a32, "peak": FP32_PEAK_TFLOPS, "frac": a32 / FP32_PEAK_TFLOPS},
-                "peak_source": "measured DFMA/FFMA microbenchmark (MEASURED_PEAKS.json has HBM and bf16 only)",
+                "composite_frac": a64 / FP64_PEAK_TFLOPS + a32 / FP32_PEAK_TFLOPS,
+                "peak_source": "measured on this pool's B200: DMMA m8n8k4 f64 36.8 TF/s (DFMA 36.2, same FP64 "
+                               "hardware), FFMA 69.7 TF/s (tools/peakbench.cu, tools/pipebench.cu; "
+                               "MEASURED_PEAKS.json has HBM and bf16 only)",
             }
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -360,7 +386,7 @@ def main():
                        "layer_counts": summ["layer_counts"], "dag_depth": summ["max_level"],
                        "l2": "flushed (256 MiB write) between steps" if needs_flush else "inputs larger than L2",
                        "parallelism": f"frames sharded x{world}" if scaling == "strong" else f"replicas x{world}"},
-            "gpu_launches": 7 * args.steps + (0 if world == 1 else 0),
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
