@@ -197,15 +197,30 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 
   // ---------------------------------------------------------------- means
   {
-    double a0 = 0.0, a1 = 0.0;
+    // 4 independent accumulator pairs per lane (loads overlap), fixed-order combine
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
     const typename ZL::Ref c0 = zv.ref(H, lane), c1 = zv.ref(H, lane < 8 ? 32 + lane : 37);
-    for (int j = warp; j < m; j += NWARP) {
-      const int b = zv.base(j);
-      a0 += zv.at(c0, b);
-      a1 += zv.at(c1, b);
+    int j = warp;
+    for (; j + 3 * NWARP < m; j += 4 * NWARP) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int b = zv.base(j + u * NWARP);
+        a0[u] += zv.at(c0, b);
+        a1[u] += zv.at(c1, b);
+      }
     }
-    H.wmin[warp][lane] = a0;
-    if (lane < 8) H.wmin[warp][32 + lane] = a1;
+#pragma unroll
+    for (int u = 0; u < 3; u++) {  // tail: j + 3 NWARP >= m
+      if (j + u * NWARP < m) {
+        const int b = zv.base(j + u * NWARP);
+        a0[u] += zv.at(c0, b);
+        a1[u] += zv.at(c1, b);
+      }
+    }
+    a0[0] = (a0[0] + a0[1]) + (a0[2] + a0[3]);
+    a1[0] = (a1[0] + a1[1]) + (a1[2] + a1[3]);
+    H.wmin[warp][lane] = a0[0];
+    if (lane < 8) H.wmin[warp][32 + lane] = a1[0];
     __syncthreads();
     if (tid < 40) {
       double s = 0.0;
@@ -691,17 +706,22 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   // so that v_i . v_j = U_i . (y0 - y_j) reads candidate j straight from the
   // shared support tile (V never goes through global memory).
   double* Un = H.R2;        // [40][LS]  A fragments of the Gram GEMM
-  double* Vt = H.R1;        // [KMAX][32] L^-1 (y0 - y_near_i) (R1 head is free here)
+  double* Vt = H.R1;             // [KMAX][32] L^-1 (y0 - y_near_i) (R1 head is free here)
+  double* Wt = H.R1 + KMAX * 32;  // [KMAX][32] y0 - y_near_i (below Zp)
+  static_assert(2 * KMAX * 32 <= ZP_OFF + KMAX * 40, "staging fits R1");
+  for (int o = tid; o < k * 32; o += NT) {
+    const int i = o >> 5, q = o & 31;
+    Wt[o] = q < n ? y0[q] - zv.at(zv.ref(H, q), zv.base(H.near[i])) : 0.0;
+  }
+  if (tid < 40) H.dn[tid] = tid < k ? dS[H.near[tid]] : 0.0;
+  __syncthreads();
   for (int o = tid; o < KMAX * 32; o += NT) {
     const int i = o >> 5, t = o & 31;
     double sv = 0.0;
-    if (i < k && t < n) {
-      const int b = zv.base(H.near[i]);
-      for (int q = 0; q <= t; q++) sv = fma(H.Linv[t * LS + q], y0[q] - zv.at(zv.ref(H, q), b), sv);
-    }
+    if (i < k && t < n)
+      for (int q = 0; q <= t; q++) sv = fma(H.Linv[t * LS + q], Wt[i * 32 + q], sv);
     Vt[i * 32 + t] = sv;
   }
-  if (tid < 40) H.dn[tid] = tid < k ? dS[H.near[tid]] : 0.0;
   __syncthreads();
   for (int o = tid; o < 40 * 32; o += NT) {
     const int i = o >> 5, t = o & 31;
@@ -843,26 +863,29 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   // ---------------------------------- alpha (estimators.py:237-245)
   {
     double* u = H.R1;  // [KMAX][32]
+    double* R = H.R2;  // [KMAX][36]: y_i - y~_i | x_i - x~_i  (Un is dead here)
+    for (int o = tid; o < k * 36; o += NT) {
+      const int i = o / 36, q = o % 36;
+      double r = 0.0;
+      if (q < n || q >= 32)
+        r = zv.at(zv.ref(H, q), zv.base(H.near[i])) - Zp[i * 40 + q] / Zp[i * 40 + ONES_COL];
+      R[o] = r;
+    }
+    __syncthreads();
     for (int o = tid; o < k * 32; o += NT) {
       const int i = o >> 5, t = o & 31;
-      const int b = zv.base(H.near[i]);
-      const double S = Zp[i * 40 + 36];
       double s = 0.0;
-      for (int q = 0; q <= t && q < n; q++) {
-        const double r = zv.at(zv.ref(H, q), b) - Zp[i * 40 + q] / S;  // y_i - y~_i
-        s = fma(H.Linv[t * LS + q], r, s);
-      }
-      u[i * 32 + t] = t < n ? s : 0.0;
+      if (t < n)
+        for (int q = 0; q <= t; q++) s = fma(H.Linv[t * LS + q], R[i * 36 + q], s);
+      u[o] = s;
     }
     __syncthreads();
     for (int o = tid; o < 4 * k; o += NT) {
       const int q = o / k, i = o % k;
       double c = 0.0;
       for (int t = 0; t < n; t++) c = fma(H.Bm[q * 32 + t], u[i * 32 + t], c);
-      const int b = zv.base(H.near[i]);
-      const double S = Zp[i * 40 + 36];
       H.cmat[q * k + i] = c;
-      H.rmat[q * k + i] = zv.at(zv.ref(H, 32 + q), b) - Zp[i * 40 + 32 + q] / S;
+      H.rmat[q * k + i] = R[i * 36 + 32 + q];
     }
     __syncthreads();
     if (warp == 0) {
