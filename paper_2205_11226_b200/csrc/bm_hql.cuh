@@ -93,6 +93,18 @@ __device__ __forceinline__ void with_na(int n, F&& f) {
   else f(IntC<4>{});
 }
 
+// Warp-wide minimum of (v, j) pairs, v >= 0 or +inf (no NaN), ties to the
+// smaller j: three redux.sync steps on the order-preserving bit pattern
+// (hi word, lo word, index) instead of a 5-round shuffle butterfly.  Returns v
+// and the winning j (all lanes).
+__device__ __forceinline__ double warp_argmin_key(double v, int j, int& jmin) {
+  const unsigned hi = (unsigned)__double2hiint(v), lo = (unsigned)__double2loint(v);
+  const unsigned mh = __reduce_min_sync(FULL, hi);
+  const unsigned ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xFFFFFFFFu);
+  jmin = (int)__reduce_min_sync(FULL, (hi == mh && lo == ml) ? (unsigned)j : 0x7FFFFFFFu);
+  return __hiloint2double((int)mh, (int)ml);
+}
+
 // Fixed-order tree reduction of per-warp register tiles (NWARP warps -> warp 0)
 // in chunks of C values; red must hold (NWARP/2) * C * 32 doubles.
 template <int N, int C = N>
@@ -457,18 +469,13 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
             ej[i + 1] = tj;
           }
         }
+      if (tid == 32) atomicAdd(&g_phase_cycles[35], (unsigned long long)(clock64() - ph_t));  // sorted (diag)
       // (2) each warp merges its 32 sorted lanes into its k smallest
       double* lv = H.R2;                           // [NWARP-1][KMAX] values
       int* lj = reinterpret_cast<int*>(H.R2 + (NWARP - 1) * KMAX);  // [NWARP-1][KMAX] indices
       for (int it = 0; it < k; it++) {
-        double bv = ev[0];
-        int bj = ej[0];
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-          const double ov = __shfl_xor_sync(FULL, bv, o);
-          const int oj = __shfl_xor_sync(FULL, bj, o);
-          if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
-        }
+        int bj;
+        const double bv = warp_argmin_key(ev[0], ej[0], bj);
         if (lane == 0) {
           lv[w7 * KMAX + it] = bv;
           lj[w7 * KMAX + it] = bj;
@@ -483,20 +490,17 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           ej[PER - 1] = 0x7fffffff;
         }
       }
+      if (tid == 32) atomicAdd(&g_phase_cycles[36], (unsigned long long)(clock64() - ph_t));  // warp merged (diag)
       asm volatile("bar.sync 1, %0;" ::"r"(NW7) : "memory");  // warps 1..NWARP-1
+      if (tid == 32) atomicAdd(&g_phase_cycles[37], (unsigned long long)(clock64() - ph_t));  // all merged (diag)
       // (3) warp 1 merges the NWARP-1 sorted lists: lane w holds list w's head
       if (w7 == 0) {
         int ptr = 0;
         for (int it = 0; it < k; it++) {
-          double bv = (lane < NWARP - 1 && ptr < k) ? lv[lane * KMAX + ptr] : INFINITY;
-          int bj = (lane < NWARP - 1 && ptr < k) ? lj[lane * KMAX + ptr] : 0x7fffffff;
-          const int myj = bj;
-#pragma unroll
-          for (int o = 16; o; o >>= 1) {
-            const double ov = __shfl_xor_sync(FULL, bv, o);
-            const int oj = __shfl_xor_sync(FULL, bj, o);
-            if (ov < bv || (ov == bv && oj < bj)) { bv = ov; bj = oj; }
-          }
+          const double hv = (lane < NWARP - 1 && ptr < k) ? lv[lane * KMAX + ptr] : INFINITY;
+          const int myj = (lane < NWARP - 1 && ptr < k) ? lj[lane * KMAX + ptr] : 0x7fffffff;
+          int bj;
+          warp_argmin_key(hv, myj, bj);
           if (lane == 0) H.near[it] = bj;
           if (myj == bj && lane < NWARP - 1) ptr++;
         }

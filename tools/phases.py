@@ -40,3 +40,5 @@ for k in ('sidl_setup', 'sidl_screen', 'sidl_ringsums', 'sidl_scan', 'sidl_dist_
     print(f"  {k:14s} {ph[k] / ns:8.0f} cycles")
 print(f"beta: loop(t0) {ph['beta_loop_t0'] / max(n_hql,1):.0f}  loop+reduce {ph['beta_loop_reduce'] / max(n_hql,1):.0f}  (phase total {ph['beta'] / max(n_hql,1):.0f})")
 print(f"loo: loops(t0) {ph['loo_loops_t0'] / max(n_hql,1):.0f}  (phase total {ph['loo'] / max(n_hql,1):.0f})")
+print("nearest (from HQL start): e2 %.0f sorted %.0f warp-merged %.0f all-merged %.0f final %.0f" % tuple(
+    ph[k] / max(n_hql, 1) for k in ("e2_done", "nn_sorted", "nn_warp_merged", "nn_all_merged", "nearest")))
