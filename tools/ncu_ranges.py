@@ -1,10 +1,15 @@
 """Dev tool: stall reasons aggregated over source-line ranges (ncu source page CSV, cuda,sass)."""
 import csv, sys
 path = sys.argv[1]
-ranges = {  # (file, lo, hi) -> name
-    ('bm_hql.cuh', 183, 203): 'means', ('bm_hql.cuh', 205, 306): 'covariance', ('bm_hql.cuh', 307, 471): 'chol+nearest',
-    ('bm_hql.cuh', 472, 546): 'quadforms', ('bm_hql.cuh', 547, 559): 'dmin', ('bm_hql.cuh', 560, 651): 'beta',
-    ('bm_hql.cuh', 652, 680): 'staging', ('bm_hql.cuh', 681, 810): 'loo', ('bm_hql.cuh', 811, 870): 'alpha',
+ranges = {  # (file, lo, hi) -> name (line anchors of the round-1 final sources)
+    ('bm_hql.cuh', 210, 246): 'hql:means', ('bm_hql.cuh', 247, 354): 'hql:covariance',
+    ('bm_hql.cuh', 355, 526): 'hql:chol+nearest', ('bm_hql.cuh', 527, 599): 'hql:quadforms+dmin',
+    ('bm_hql.cuh', 600, 704): 'hql:beta', ('bm_hql.cuh', 705, 739): 'hql:staging',
+    ('bm_hql.cuh', 740, 866): 'hql:loo', ('bm_hql.cuh', 867, 925): 'hql:alpha',
+    ('bm_conceal.cu', 294, 336): 'sched_pop', ('bm_conceal.cu', 337, 388): 'load_tile',
+    ('bm_conceal.cu', 389, 471): 'gate:screen_chunk', ('bm_conceal.cu', 472, 629): 'gate:gather',
+    ('bm_conceal.cu', 648, 822): 'estimate_patch', ('bm_conceal.cu', 823, 884): 'pick_and_extract',
+    ('bm_conceal.cu', 885, 1035): 'k_conceal loop',
 }
 rows = list(csv.reader(open(path)))
 hdr = next(r for r in rows if r and r[0] == 'Line No')
