@@ -120,6 +120,34 @@ void bm_kernel_times_reset(void);
 /* Diagnostics: 40 cumulative SM-cycle counters (HQL phases, IDL patch
  * phases, scheduling); names in _native.PHASES. */
 int bm_debug_phase_cycles(unsigned long long* out40, int reset);
+/* ---- callers either side of the path ---------- */
+
+/* Batched squared-error sums for PSNR (metrics.py:50-75): per frame,
+ * out_sum[f] = sum over selected pixels of (ref - test)^2 (FP64) and
+ * out_count[f] = number of selected pixels; select = NULL selects all (psnr),
+ * else a u8 [B,H,W] 0/1 selection (psnr_masked, e.g. the originally lost set).
+ * Device pointers; PSNR = 10 log10(255^2 / (sum / count)) on the host. */
+int bm_sqdiff_batch(const void* ref, const void* test, int pixel_dtype, const uint8_t* select, int frames,
+                    int height, int width, double* out_sum, double* out_count, void* stream);
+/* Batched mean SSIM (metrics.py:86-116): 11x11 Gaussian window (sigma 1.5),
+ * K1 0.01, K2 0.03, L 255, windows fully inside the frame, FP64.
+ * out_mean[f] (device).  BM_ERR_ARGS when a side is < 11 (ValueError). */
+int bm_ssim_batch(const void* ref, const void* test, int pixel_dtype, int frames, int height, int width,
+                  double* out_mean, void* stream);
+/* Loss-pattern generation on the device (loss.py:24-77), bit-identical to the
+ * reference generators: writes PixelState values (0 AVAILABLE, 1 LOST) into
+ * out_states [B,H,W].  BM_MASK_DISPERSED: blocks with odd row and odd column
+ * (gen_dispersed_mask); BM_MASK_RANDOM: exactly `count` blocks, the first
+ * `count` of a SplitMix64(seeds[f]) Fisher-Yates shuffle of the block indices
+ * (gen_random_mask with count = round_half_up(rate * blocks)); BM_MASK_SLICE:
+ * `count` whole block rows, the first of a Fisher-Yates shuffle of the rows
+ * (the BASELINE slice-loss pattern).  seeds: device u64 [B]. */
+#define BM_MASK_DISPERSED 0
+#define BM_MASK_RANDOM 1
+#define BM_MASK_SLICE 2
+int bm_gen_masks(int kind, int frames, int height, int width, int block_size, int count, const uint64_t* seeds,
+                 uint8_t* out_states, void* stream);
+
 /* SM clock of the current device in kHz (converts bm_patch_record.cycles to
  * seconds for ConcealmentReport.patch_times); 0 when no device. */
 int bm_device_clock_khz(void);

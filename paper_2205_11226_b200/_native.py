@@ -16,7 +16,7 @@ from .errors import DimensionMismatchError, NativeUnavailableError
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
-SOURCES = [os.path.join(PKG_DIR, "csrc", "bm_conceal.cu")]
+SOURCES = [os.path.join(PKG_DIR, "csrc", "bm_conceal.cu"), os.path.join(PKG_DIR, "csrc", "bm_aux.cu")]
 HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh"))) + [
     os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
 ]
@@ -65,6 +65,7 @@ EXPORTS = [
     "bm_abi_version", "bm_status_string", "bm_workspace_bytes", "bm_max_records", "bm_device_clock_khz",
     "bm_kernel_times_ms", "bm_kernel_times_reset", "bm_debug_phase_cycles",
     "bm_conceal", "bm_compact_records", "bm_conceal_host", "bm_estimate_batch",
+    "bm_sqdiff_batch", "bm_ssim_batch", "bm_gen_masks",
 ]
 
 
@@ -128,6 +129,12 @@ def lib():
     L.bm_conceal_host.argtypes = [ctypes.POINTER(Params), vp, vp, vp, vp, vp, ctypes.POINTER(i64), ctypes.POINTER(Summary)]
     L.bm_estimate_batch.restype = ctypes.c_int
     L.bm_estimate_batch.argtypes = [i32, i32, i32, ctypes.c_double, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.bm_sqdiff_batch.restype = ctypes.c_int
+    L.bm_sqdiff_batch.argtypes = [vp, vp, i32, vp, i32, i32, i32, vp, vp, vp]
+    L.bm_ssim_batch.restype = ctypes.c_int
+    L.bm_ssim_batch.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
+    L.bm_gen_masks.restype = ctypes.c_int
+    L.bm_gen_masks.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, vp]
     _lib = L
     return L
 
