@@ -859,20 +859,32 @@ __device__ void pick_and_extract(CellSmem& S) {
     E.y0f[idx] = S.tile32[o];
     E.uoff[idx] = (int16_t)(ctx_r(lane) * TS + ctx_c(lane));
   }
-  // row masks of used window positions (usable context + patch cells)
-  unsigned rm = 0;
-  if (lane < 6) {
-    for (int k = 0; k < 32; k++)
-      if (((bal >> k) & 1u) && ctx_r(k) == lane) rm |= 1u << ctx_c(k);
-    if (lane == 2 || lane == 3) rm |= (1u << 2) | (1u << 3);
-    S.rowmask[lane] = rm;
+  // row masks of used window positions (usable context + patch cells): one
+  // redux.or per window row
+  const unsigned mybit = usable ? 1u << ctx_c(lane) : 0u;
+#pragma unroll
+  for (int q = 0; q < 6; q++) {
+    unsigned rm = __reduce_or_sync(FULL, ctx_r(lane) == q ? mybit : 0u);
+    if (q == 2 || q == 3) rm |= (1u << 2) | (1u << 3);
+    if (lane == q) S.rowmask[q] = rm;
   }
-  __syncwarp();
   if (lane < 4) E.uoff[n + lane] = (int16_t)((2 + (lane >> 1)) * TS + 2 + (lane & 1));
-  // flatness (profiles.py:98-102)
-  double ymax = usable ? S.tile[o] : -INFINITY, ymin = usable ? S.tile[o] : INFINITY;
-  ymax = warp_max(ymax);
-  ymin = warp_min(ymin);
+  // flatness (profiles.py:98-102): exact max / min of y0 by redux on
+  // order-preserving 64-bit keys (hi word, then lo word)
+  const double yv = usable ? S.tile[o] : 0.0;
+  const unsigned long long ub = (unsigned long long)__double_as_longlong(yv);
+  const unsigned long long key = (ub >> 63) ? ~ub : (ub | 0x8000000000000000ull);
+  const unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+  const unsigned mxh = __reduce_max_sync(FULL, usable ? khi : 0u);
+  const unsigned mxl = __reduce_max_sync(FULL, usable && khi == mxh ? klo : 0u);
+  const unsigned mnh = __reduce_min_sync(FULL, usable ? khi : 0xFFFFFFFFu);
+  const unsigned mnl = __reduce_min_sync(FULL, usable && khi == mnh ? klo : 0xFFFFFFFFu);
+  auto unkey = [](unsigned h, unsigned l) {
+    const unsigned long long k = ((unsigned long long)h << 32) | l;
+    return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
+  };
+  const double ymax = unkey(mxh, mxl), ymin = unkey(mnh, mnl);
+  __syncwarp();
   if (lane == 0) {
     S.pick = p;
     S.pend = pend & ~(1ull << p);
