@@ -41,15 +41,28 @@ __device__ __forceinline__ float warp_sumf(float v) {
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
   return v;
 }
-__device__ __forceinline__ double warp_min(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL, v, o));
-  return v;
+// Exact warp max / min of doubles with two redux.sync steps on an
+// order-preserving 64-bit key (hi word, then lo word) instead of a 5-round
+// shuffle butterfly.  NaN lanes are ignored (like fmax / fmin).
+__device__ __forceinline__ unsigned long long f64_key(double v) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double f64_unkey(unsigned hi, unsigned lo) {
+  const unsigned long long k = ((unsigned long long)hi << 32) | lo;
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k));
 }
 __device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
-  return v;
+  const unsigned long long k = f64_key(v != v ? -INFINITY : v);
+  const unsigned h = __reduce_max_sync(FULL, (unsigned)(k >> 32));
+  const unsigned l = __reduce_max_sync(FULL, (unsigned)(k >> 32) == h ? (unsigned)k : 0u);
+  return f64_unkey(h, l);
+}
+__device__ __forceinline__ double warp_min(double v) {
+  const unsigned long long k = f64_key(v != v ? INFINITY : v);
+  const unsigned h = __reduce_min_sync(FULL, (unsigned)(k >> 32));
+  const unsigned l = __reduce_min_sync(FULL, (unsigned)(k >> 32) == h ? (unsigned)k : 0xFFFFFFFFu);
+  return f64_unkey(h, l);
 }
 __device__ __forceinline__ float warp_minf(float v) {
 #pragma unroll
@@ -57,9 +70,7 @@ __device__ __forceinline__ float warp_minf(float v) {
   return v;
 }
 __device__ __forceinline__ int warp_sumi(int v) {
-#pragma unroll
-  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
+  return (int)__reduce_add_sync(FULL, (unsigned)v);
 }
 
 // Transposing warp reduction: every lane holds v[0..31]; afterwards lane l
