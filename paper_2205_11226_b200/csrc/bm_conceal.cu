@@ -699,7 +699,7 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     const int mode = (gated && !(S.nu < P.t_nu)) ? 0 : (forced == BM_LAYER_IDL ? 1 : 2);
     bool done = false;
     if (mode == 2 && m >= 2) {
-      if (tid == 0) atomicAdd(&g_phase_cycles[0], (unsigned long long)(clock64() - S.t_start));
+      if (tid == 0) BM_DIAG_ADD(0, (clock64() - S.t_start));
       hql_columns(S.hql, E.n, E.uoff);
       __syncthreads();
       TileLoader zv{S.tile, S.cand};
@@ -726,19 +726,19 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     }
     if (mode == 0) {
       if (tid == 0 && m < 64) {  // small-m IDL patches: gather / estimate sub-phases
-        atomicAdd(&g_phase_cycles[24], (unsigned long long)(S.t_g[0] - (S.t_mark - S.t_gather)));
-        atomicAdd(&g_phase_cycles[25], (unsigned long long)(S.t_g[1] - S.t_g[0]));
-        atomicAdd(&g_phase_cycles[26], (unsigned long long)(S.t_g[2] - S.t_g[1]));
-        atomicAdd(&g_phase_cycles[27], (unsigned long long)(S.t_g[3] - S.t_g[2]));
-        atomicAdd(&g_phase_cycles[28], (unsigned long long)(E.t_e[0] - S.t_g[3]));
-        atomicAdd(&g_phase_cycles[29], (unsigned long long)(E.t_e[1] - E.t_e[0]));
-        atomicAdd(&g_phase_cycles[30], (unsigned long long)(clock64() - E.t_e[1]));
-        atomicAdd(&g_phase_cycles[31], 1ull);
+        BM_DIAG_ADD(24, (S.t_g[0] - (S.t_mark - S.t_gather)));
+        BM_DIAG_ADD(25, (S.t_g[1] - S.t_g[0]));
+        BM_DIAG_ADD(26, (S.t_g[2] - S.t_g[1]));
+        BM_DIAG_ADD(27, (S.t_g[3] - S.t_g[2]));
+        BM_DIAG_ADD(28, (E.t_e[0] - S.t_g[3]));
+        BM_DIAG_ADD(29, (E.t_e[1] - E.t_e[0]));
+        BM_DIAG_ADD(30, (clock64() - E.t_e[1]));
+        BM_DIAG_ADD(31, 1);
       }
       if (tid == 0) {
-        atomicAdd(&g_phase_cycles[16], (unsigned long long)S.t_pick);
-        atomicAdd(&g_phase_cycles[17], (unsigned long long)S.t_gather);
-        atomicAdd(&g_phase_cycles[18], (unsigned long long)(clock64() - S.t_mark));
+        BM_DIAG_ADD(16, S.t_pick);
+        BM_DIAG_ADD(17, S.t_gather);
+        BM_DIAG_ADD(18, (clock64() - S.t_mark));
         S.t_mark = clock64();
         S.idl_diag = 1;
         rec.layer = BM_LAYER_IDL;
@@ -806,12 +806,12 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
   }
   if (tid == 0) {
     if (S.idl_diag) {
-      atomicAdd(&g_phase_cycles[19], (unsigned long long)(clock64() - S.t_mark));
+      BM_DIAG_ADD(19, (clock64() - S.t_mark));
       S.idl_diag = 0;
     }
     rec.cycles = (uint32_t)(clock64() - S.t_start);
-    if (rec.layer >= BM_LAYER_IDL) atomicAdd(&g_phase_cycles[13 + rec.layer], (unsigned long long)rec.cycles);
-    else atomicAdd(&g_phase_cycles[21], (unsigned long long)rec.cycles);
+    if (rec.layer >= BM_LAYER_IDL) BM_DIAG_ADD(13 + rec.layer, rec.cycles);
+    else BM_DIAG_ADD(21, rec.cycles);
     write_record(P, S, rec);
     S.nrec++;
     S.cnt[rec.layer]++;
@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
       S.gc = rem % P.GC;
     }
     __syncthreads();
-    if (tid == 0) atomicAdd(&g_phase_cycles[20], (unsigned long long)(clock64() - t_w0));  // scheduling wait
+    if (tid == 0) BM_DIAG_ADD(20, (clock64() - t_w0));  // scheduling wait
     load_tile(P, S);
     // lost_patch_origins (framework.py:219-227)
     if (tid < 32) {
@@ -1046,8 +1046,8 @@ __global__ void __launch_bounds__(NT, 2) k_conceal(KParams P) {
   }
   __syncthreads();
   if (tid == 0) {
-    atomicAdd(&g_phase_cycles[22], (unsigned long long)(clock64() - t_cta0));  // CTA lifetime
-    atomicAdd(&g_phase_cycles[23], 1ull);
+    BM_DIAG_ADD(22, (clock64() - t_cta0));  // CTA lifetime
+    BM_DIAG_ADD(23, 1);
   }
   if (tid < 4 && S.cnt[tid]) atomicAdd(&P.counters[tid], S.cnt[tid]);
   if (tid >= 4 && tid < 8 && S.cnt[tid]) atomicAdd(&P.counters[tid + 4], S.cnt[tid]);

@@ -72,9 +72,8 @@ struct HqlSmem {
 };
 
 // per-CTA global scratch (doubles)
-constexpr size_t HQL_E2 = 0;
-constexpr size_t HQL_Z = HQL_E2 + (size_t)MAXCAND * 16;       // dense Z [MAXCAND][40] (estimator API only)
-constexpr size_t HQL_SCRATCH_FUSED = HQL_Z;
+constexpr size_t HQL_Z = 0;                                   // dense Z [MAXCAND][40] (estimator API only)
+constexpr size_t HQL_SCRATCH_FUSED = 0;                       // the fused kernel needs none
 constexpr size_t HQL_SCRATCH_DENSE = HQL_Z + (size_t)MAXCAND * 40;
 
 // Dispatch on the number of 8-wide column tiles that hold the n used context
@@ -177,17 +176,26 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
 
 // The HQL pipeline for one patch.  Inputs: zv (candidates), m >= 2, n, y0
 // (shared, [32]).  Outputs in H/out: ok, vals[4], beta, alpha, gap.
-// Per-phase cycle accounting of the HQL pipeline (thread 0, after barriers);
-// read back with bm_debug_phase_cycles.  Phase 0 = everything before HQL.
+// Per-phase cycle accounting of the HQL pipeline and the patch loop (thread 0,
+// after barriers); read back with bm_debug_phase_cycles.  Phase 0 =
+// everything before HQL.  Compiled in only for diagnostic builds
+// (-DBM_DIAG=1: tools/build_variant.sh + BM_NATIVE_VARIANT); the product
+// build carries no per-patch global atomics.
 __device__ unsigned long long g_phase_cycles[40];
-#define BM_PHASE(k)                                                    \
-  do {                                                                 \
-    if (threadIdx.x == 0) {                                            \
-      const long long now_ = clock64();                                \
-      atomicAdd(&g_phase_cycles[k], (unsigned long long)(now_ - ph_t)); \
-      ph_t = now_;                                                     \
-    }                                                                  \
+#if BM_DIAG
+#define BM_DIAG_ADD(k, v) atomicAdd(&g_phase_cycles[k], (unsigned long long)(v))
+#define BM_PHASE(k)                                 \
+  do {                                              \
+    if (threadIdx.x == 0) {                         \
+      const long long now_ = clock64();             \
+      BM_DIAG_ADD(k, now_ - ph_t);                  \
+      ph_t = now_;                                  \
+    }                                               \
   } while (0)
+#else
+#define BM_DIAG_ADD(k, v) ((void)0)
+#define BM_PHASE(k) ((void)0)
+#endif
 
 struct HqlOut {
   double vals[4];
@@ -201,8 +209,6 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
                         HqlOut& out, const double* exptab, double* dS) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  double* gE2P = gs + HQL_E2;                 // [MAXCAND][8] pairwise accumulators r[g]
-  double* gE2T = gE2P + (size_t)MAXCAND * 8;  // [MAXCAND][8] tail squares
   long long ph_t = clock64();
   const int nks = (m + 3) >> 2;  // k-steps of 4 candidates
   const int nct = (m + 7) >> 3;  // column tiles of 8 candidates
@@ -257,26 +263,14 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     double acc[28];
 #pragma unroll
     for (int i = 0; i < 28; i++) acc[i] = 0.0;
-    // software pipeline: the next k-step's fragments load during this step's
-    // MMAs.  The same raw values also give the candidate's Euclidean distance
-    // to y0 in NumPy's pairwise order (optimize_alpha's nearest set,
-    // estimators.py:222): lane (g,t4) holds dims g, g+8, g+16, g+24 of
-    // candidate 4s+t4 = exactly NumPy's r[g] accumulator; the xor-4/8/16
-    // butterfly is its ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree; the n % 8 tail
-    // dims are added sequentially afterwards.
-    const int n8 = n - (n % 8), ntail = n - n8;
-    double y0g[4];
-#pragma unroll
-    for (int tl = 0; tl < 4; tl++) y0g[tl] = 8 * tl + g < n ? y0[8 * tl + g] : 0.0;
+    // software pipeline: the next k-step's fragments load during this step's MMAs
     with_na(n, [&](auto NAc) {
     constexpr int NA = decltype(NAc)::value;
-    double f[5], fn[5], e2p, e2n, tq, tqn;
-    auto load_f = [&](int s, double(&o)[5], double& ep, double& tsq) {
+    double f[5], fn[5];
+    auto load_f = [&](int s, double(&o)[5]) {
       const int j = 4 * s + t4;
       const bool valid = j < m;
       const int b = zv.base(min(j, m - 1));  // clamped: branch-free loads
-      double r = 0.0;
-      tsq = 0.0;
 #pragma unroll
       for (int tl = 0; tl < 5; tl++) {
         if (tl >= NA && tl < 4) {
@@ -285,28 +279,12 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         }
         const double raw = zv.at(cr[tl], b);
         o[tl] = valid ? raw - mu[tl] : 0.0;
-        if (tl < 4) {
-          const double d = raw - y0g[tl];
-          const double sq = __dmul_rn(d, d);
-          if (8 * tl + g < n8) r = __dadd_rn(r, sq);
-          if (8 * tl == n8) tsq = sq;  // tail dim n8 + g (valid if g < ntail)
-        }
-      }
-      ep = r;
-    };
-    // partial sums leave the loop through L2; the tree + tail is done per
-    // candidate by the nearest-set warps (keeps shuffles off the MMA path)
-    auto finish_e2 = [&](int s, double r, double tsq) {
-      const int j = 4 * s + t4;
-      if (j < m) {
-        gE2P[j * 8 + g] = r;
-        gE2T[j * 8 + g] = tsq;
       }
     };
-    load_f(warp, f, e2p, tq);
+    load_f(warp, f);
 #pragma unroll 1
     for (int s = warp; s < nks; s += NWARP) {
-      load_f(s + NWARP, fn, e2n, tqn);
+      load_f(s + NWARP, fn);
       int idx = 0;
 #pragma unroll
       for (int a = 0; a < 4; a++)
@@ -315,11 +293,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           if (a < NA && (bb < NA || bb == 4)) dmma(acc[2 * idx], acc[2 * idx + 1], f[a], f[bb]);
           idx++;
         }
-      finish_e2(s, e2p, tq);
 #pragma unroll
       for (int tl = 0; tl < 5; tl++) f[tl] = fn[tl];
-      e2p = e2n;
-      tq = tqn;
     }
     });
     tree_reduce<28, 14>(acc, H.R1);
@@ -411,7 +386,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       __syncwarp();
       if (lane == 0) {
         H.fail = fail;
-        atomicAdd(&g_phase_cycles[13], (unsigned long long)(clock64() - ph_t));  // Cholesky alone (diagnostic)
+        BM_DIAG_ADD(13, (clock64() - ph_t));  // Cholesky alone (diagnostic)
       }
       // L^-1 in registers: lane c builds column c by forward substitution
       // (L rows read as shared-memory broadcasts); identity beyond n
@@ -436,20 +411,36 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       constexpr int NW7 = NT - 32, PER = (MAXCAND + NW7 - 1) / NW7;
       const int t7 = tid - 32, w7 = warp - 1;
       double ev[PER];
-      const int n8 = n - (n % 8), ntail = n - n8;
+      // dist2 = ((y - y0) ** 2).sum(axis=1) in NumPy's pairwise order: eight
+      // strided accumulators r[g] (dims g, g+8, ...) below n8 = n - n % 8, the
+      // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree, then the tail dims in order
+      // (n < 8: tail only).  One candidate per thread, read from the tile.
+      // Column refs and y0 are shared-memory broadcasts.
+      const int n8 = n - (n % 8);
 #pragma unroll
       for (int i = 0; i < PER; i++) {
         const int j = t7 + i * NW7;
         ev[i] = INFINITY;
-        if (j < m) {  // NumPy pairwise tree over the covariance pass's partial sums
-          const double* r = gE2P + j * 8;
-          const double* t = gE2T + j * 8;
-          double e = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-          for (int q = 0; q < ntail; q++) e = __dadd_rn(e, t[q]);
+        if (j < m) {
+          const int b = zv.base(j);
+          auto sq = [&](int q) {
+            const double d = __dsub_rn(zv.at(zv.ref(H, q), b), y0[q]);
+            return __dmul_rn(d, d);
+          };
+          double r[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) r[q] = 0.0;
+#pragma unroll 1
+          for (int q0 = 0; q0 < n8; q0 += 8)
+#pragma unroll
+            for (int q = 0; q < 8; q++) r[q] = __dadd_rn(r[q], sq(q0 + q));
+          double e = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                               __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll 1
+          for (int q = n8; q < n; q++) e = __dadd_rn(e, sq(q));
           ev[i] = e;
         }
       }
-      if (tid == 32) atomicAdd(&g_phase_cycles[10], (unsigned long long)(clock64() - ph_t));  // e2 done (diagnostic)
       const int k = min(n + 1, m);
       // (1) per-thread sort of its PER candidates by (e2, index)
       int ej[PER];
@@ -469,7 +460,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
             ej[i + 1] = tj;
           }
         }
-      if (tid == 32) atomicAdd(&g_phase_cycles[35], (unsigned long long)(clock64() - ph_t));  // sorted (diag)
+      if (tid == 32) BM_DIAG_ADD(35, (clock64() - ph_t));  // sorted (diag)
       // (2) each warp merges its 32 sorted lanes into its k smallest
       double* lv = H.R2;                           // [NWARP-1][KMAX] values
       int* lj = reinterpret_cast<int*>(H.R2 + (NWARP - 1) * KMAX);  // [NWARP-1][KMAX] indices
@@ -490,9 +481,9 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           ej[PER - 1] = 0x7fffffff;
         }
       }
-      if (tid == 32) atomicAdd(&g_phase_cycles[36], (unsigned long long)(clock64() - ph_t));  // warp merged (diag)
+      if (tid == 32) BM_DIAG_ADD(36, (clock64() - ph_t));  // warp merged (diag)
       asm volatile("bar.sync 1, %0;" ::"r"(NW7) : "memory");  // warps 1..NWARP-1
-      if (tid == 32) atomicAdd(&g_phase_cycles[37], (unsigned long long)(clock64() - ph_t));  // all merged (diag)
+      if (tid == 32) BM_DIAG_ADD(37, (clock64() - ph_t));  // all merged (diag)
       // (3) warp 1 merges the NWARP-1 sorted lists: lane w holds list w's head
       if (w7 == 0) {
         int ptr = 0;
@@ -504,7 +495,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           if (lane == 0) H.near[it] = bj;
           if (myj == bj && lane < NWARP - 1) ptr++;
         }
-        if (lane == 0) atomicAdd(&g_phase_cycles[8], (unsigned long long)(clock64() - ph_t));  // nearest side (diagnostic)
+        if (lane == 0) BM_DIAG_ADD(8, (clock64() - ph_t));  // nearest side (diagnostic)
       }
     }
     __syncthreads();
@@ -644,9 +635,9 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       for (int ct = 0; ct < 5; ct++) fb[ct] = fbn[ct];
     }
     });
-    if (tid == 0) atomicAdd(&g_phase_cycles[32], (unsigned long long)(clock64() - ph_t));  // beta loop (thread 0)
+    if (tid == 0) BM_DIAG_ADD(32, (clock64() - ph_t));  // beta loop (thread 0)
     tree_reduce<30, RED_CHUNK>(acc, H.R1);
-    if (tid == 0) atomicAdd(&g_phase_cycles[33], (unsigned long long)(clock64() - ph_t));  // beta loop + reduce
+    if (tid == 0) BM_DIAG_ADD(33, (clock64() - ph_t));  // beta loop + reduce
     constexpr int PS = 41;  // row stride of P: conflict-free per-lane row reads
     double* P = H.R2;       // [24][PS]
     if (warp == 0) {
@@ -829,7 +820,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
     }
     });
-    if (tid == 0) atomicAdd(&g_phase_cycles[34], (unsigned long long)(clock64() - t_pass));  // LOO loops (thread 0)
+    if (tid == 0) BM_DIAG_ADD(34, (clock64() - t_pass));  // LOO loops (thread 0)
     // combine the warps' partial sums at a common per-row reference
 #pragma unroll
     for (int rr = 0; rr < RR; rr++)
