@@ -119,7 +119,7 @@ int bm_kernel_times_ms(float* out, int cap);
 void bm_kernel_times_reset(void);
 /* Diagnostics: 40 cumulative SM-cycle counters (HQL phases, IDL patch
  * phases, scheduling); names in _native.PHASES. */
-int bm_debug_phase_cycles(unsigned long long* out40, int reset);
+int bm_debug_phase_cycles(unsigned long long* out48, int reset);
 /* ---- callers either side of the path ---------- */
 
 /* Batched squared-error sums for PSNR (metrics.py:50-75): per frame,

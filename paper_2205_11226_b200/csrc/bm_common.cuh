@@ -8,7 +8,10 @@
 
 namespace bm {
 
-constexpr int NT = 256;          // threads per concealment CTA (2 CTAs = 2 cells per SM, 128 regs)
+#ifndef BM_NT
+#define BM_NT 256
+#endif
+constexpr int NT = BM_NT;        // threads per concealment CTA (2 CTAs = 2 cells per SM, 128 regs)
 constexpr int NWARP = NT / 32;
 constexpr int BS = 16;           // BLOCK_SIZE (image.py:18)
 constexpr int TILE = 48;         // 3x3-cell support area (framework.py:119-127)

@@ -1296,11 +1296,11 @@ extern "C" {
 
 int bm_abi_version(void) { return BM_ABI_VERSION; }
 
-int bm_debug_phase_cycles(unsigned long long* out40, int reset) {
-  if (cudaMemcpyFromSymbol(out40, g_phase_cycles, 40 * 8) != cudaSuccess) return BM_ERR_CUDA;
+int bm_debug_phase_cycles(unsigned long long* out48, int reset) {
+  if (cudaMemcpyFromSymbol(out48, g_phase_cycles, 48 * 8) != cudaSuccess) return BM_ERR_CUDA;
   if (reset) {
-    unsigned long long z[40] = {0};
-    cudaMemcpyToSymbol(g_phase_cycles, z, 40 * 8);
+    unsigned long long z[48] = {0};
+    cudaMemcpyToSymbol(g_phase_cycles, z, 48 * 8);
   }
   return BM_OK;
 }

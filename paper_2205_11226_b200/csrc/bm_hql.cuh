@@ -181,7 +181,7 @@ __device__ __forceinline__ void hql_columns(HqlSmem& H, int n, const int16_t* uo
 // everything before HQL.  Compiled in only for diagnostic builds
 // (-DBM_DIAG=1: tools/build_variant.sh + BM_NATIVE_VARIANT); the product
 // build carries no per-patch global atomics.
-__device__ unsigned long long g_phase_cycles[40];
+__device__ unsigned long long g_phase_cycles[48];
 #if BM_DIAG
 #define BM_DIAG_ADD(k, v) atomicAdd(&g_phase_cycles[k], (unsigned long long)(v))
 #define BM_PHASE(k)                                 \

@@ -42,3 +42,4 @@ print(f"beta: loop(t0) {ph['beta_loop_t0'] / max(n_hql,1):.0f}  loop+reduce {ph[
 print(f"loo: loops(t0) {ph['loo_loops_t0'] / max(n_hql,1):.0f}  (phase total {ph['loo'] / max(n_hql,1):.0f})")
 print("nearest (from HQL start): e2 %.0f sorted %.0f warp-merged %.0f all-merged %.0f final %.0f" % tuple(
     ph[k] / max(n_hql, 1) for k in ("e2_done", "nn_sorted", "nn_warp_merged", "nn_all_merged", "nearest")))
+print(f"per-patch cycles: IDL {ph['patch_idl'] / max(nidl, 1):.0f}  HQL {ph['patch_hql'] / max(n_hql, 1):.0f}  BRL {ph['patch_brl'] / max(r.summary['layer_counts']['BRL'], 1):.0f}")
