@@ -117,29 +117,6 @@ __device__ __forceinline__ void brl_values(EstSmem& S) {
 }
 
 // ----------------------------------------------------------------------- IDL
-// Pairwise (NumPy) sum of v[i]^2 for i < n with v in registers.
-__device__ __forceinline__ double pairwise_sq32(const double (&v)[32], int n) {
-  if (n < 8) {
-    double res = 0.0;
-#pragma unroll
-    for (int i = 0; i < 8; i++)
-      if (i < n) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
-    return res;
-  }
-  const int n8 = n - (n % 8);
-  double r[8];
-#pragma unroll
-  for (int j = 0; j < 8; j++) r[j] = __dmul_rn(v[j], v[j]);
-#pragma unroll
-  for (int i = 8; i < 32; i++)
-    if (i < n8) r[i & 7] = __dadd_rn(r[i & 7], __dmul_rn(v[i], v[i]));
-  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-#pragma unroll
-  for (int i = 8; i < 32; i++)
-    if (i >= n8 && i < n) res = __dadd_rn(res, __dmul_rn(v[i], v[i]));
-  return res;
-}
-
 // idl_weights / idl_estimate (estimators.py:112-132) in FP64, mirroring the
 // reference's arithmetic: d2 in NumPy's pairwise order, expo = -d2/(2 s2 N_y),
 // w = exp(expo - max) / sum, values = w @ x.  (The FP32 Nadaraya-Watson
@@ -157,10 +134,28 @@ __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double s
   double emax = -INFINITY;
 #pragma unroll 1
   for (int j = threadIdx.x; j < m; j += NT) {
-    double v[32];
+    // d2 = ((y - y0) ** 2).sum(axis=1) in NumPy's pairwise order, rolled:
+    // eight strided accumulators below n8, their tree, then the tail in order
+    const int n8 = n - (n % 8);
+    double r[8];
 #pragma unroll
-    for (int t = 0; t < 32; t++) v[t] = t < n ? acc.y(j, t) - S.y0[t] : 0.0;
-    const double e = -pairwise_sq32(v, n) / c;  // expo = -d2 / (2 sigma2 N_y)
+    for (int q = 0; q < 8; q++) r[q] = 0.0;
+#pragma unroll 1
+    for (int t = 0; t < n8; t += 8) {
+#pragma unroll
+      for (int q = 0; q < 8; q++) {
+        const double d = acc.y(j, t + q) - S.y0[t + q];
+        r[q] = __dadd_rn(r[q], __dmul_rn(d, d));
+      }
+    }
+    double d2 = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll 1
+    for (int t = n8; t < n; t++) {
+      const double d = acc.y(j, t) - S.y0[t];
+      d2 = __dadd_rn(d2, __dmul_rn(d, d));
+    }
+    const double e = -d2 / c;  // expo = -d2 / (2 sigma2 N_y)
     exbuf[j] = e;
     emax = fmax(emax, e);
   }

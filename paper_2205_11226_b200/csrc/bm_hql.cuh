@@ -38,6 +38,15 @@ __device__ __forceinline__ double ld_shared_f64(uint32_t a) {
 }
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
+#ifndef BM_CNEAR
+#define BM_CNEAR 1  // compact (rolled) per-patch code paths; 0 = the unrolled versions (A/B)
+#endif
+#ifndef BM_CTREE
+#define BM_CTREE 1
+#endif
+#ifndef BM_CBETA
+#define BM_CBETA 1
+#endif
 constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (36 = 4 mod 16)
 #ifndef LOO_RR
 #define LOO_RR 1  // 8-row tiles of the nearest set per LOO pass over the candidates
@@ -111,7 +120,11 @@ __device__ __forceinline__ void tree_reduce(double (&acc)[N], double* red) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int c0 = 0; c0 < N; c0 += C) {
+#if BM_CTREE
+#pragma unroll 1  // rolled over the levels: one copy of the chunk code
+#else
 #pragma unroll
+#endif
     for (int half = NWARP / 2; half >= 1; half >>= 1) {
       __syncthreads();
       if (warp >= half && warp < 2 * half) {
@@ -417,10 +430,18 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // (n < 8: tail only).  One candidate per thread, read from the tile.
       // Column refs and y0 are shared-memory broadcasts.
       const int n8 = n - (n % 8);
+#if BM_CNEAR
+      // rolled over the thread's candidates (compact code); each thread
+      // stages its own distances in dS (free until the quadforms)
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
       for (int i = 0; i < PER; i++) {
         const int j = t7 + i * NW7;
+#if !BM_CNEAR
         ev[i] = INFINITY;
+#endif
         if (j < m) {
           const int b = zv.base(j);
           auto sq = [&](int q) {
@@ -438,9 +459,20 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
                                __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
 #pragma unroll 1
           for (int q = n8; q < n; q++) e = __dadd_rn(e, sq(q));
+#if BM_CNEAR
+          dS[j] = e;
+#else
           ev[i] = e;
+#endif
         }
       }
+#if BM_CNEAR
+#pragma unroll
+      for (int i = 0; i < PER; i++) {
+        const int j = t7 + i * NW7;
+        ev[i] = j < m ? dS[j] : INFINITY;
+      }
+#endif
       const int k = min(n + 1, m);
       // (1) per-thread sort of its PER candidates by (e2, index)
       int ej[PER];
@@ -656,10 +688,22 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       double eps = INFINITY;
       if (lane < NBETA) {
         const double S = P[lane * PS + ONES_COL];
+#if BM_CBETA
+        // squares staged per lane (R1 is free after the reduction): one copy
+        // of the division code instead of one per unrolled pairwise term
+        double* sq = H.R1 + lane * 33;
+#pragma unroll 1
+        for (int t = 0; t < n; t++) {
+          const double d = y0[t] - P[lane * PS + t] / S;
+          sq[t] = __dmul_rn(d, d);
+        }
+        eps = pairwise_sum_n(n, [&](int t) { return sq[t]; });
+#else
         eps = pairwise_sum_n(n, [&](int t) {
           const double d = y0[t] - P[lane * PS + t] / S;
           return __dmul_rn(d, d);
         });
+#endif
       }
       // first minimum (ties -> smaller beta; NaN never wins), butterfly over (key, index)
       double bv = eps != eps ? INFINITY : eps;
