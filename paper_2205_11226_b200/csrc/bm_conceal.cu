@@ -66,6 +66,8 @@ struct KParams {
   int sms;             // SM count: CTAs >= sms step aside for narrow DAGs
 };
 
+constexpr int GH = 2, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
+
 struct CellSmem {
   double tile[TILE * TS];
   float tile32[TILE * TS];
@@ -73,6 +75,7 @@ struct CellSmem {
   uint64_t availbits[TILE];
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
+  uint16_t posbuf[GH * NT];  // screen_chunk: window positions of the chunk's entries
   union {
     float rbuf[MAXCAND];   // gate: per expansion-map entry nu weight, -1 = not admissible
     double dbuf[MAXCAND];  // HQL: d_j = |L^-1 (y0 - y_j)|^2
@@ -386,20 +389,38 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
 // estimators.py:105-109), ordered ballot compaction into S.cand after the
 // m_total candidates already gathered.  r is stored per entry in S.rbuf
 // (-1 = not admissible).  Returns the chunk's admissible count (all threads).
-constexpr int GH = 2, GCH = GH * NT;  // entries per chunk: GH per thread
+// nu screening weight of the admissible window at tile position pos: FP32
+// Nadaraya-Watson distance and weight (raw_idl_weights, estimators.py:105-109).
+__device__ __forceinline__ float nu_weight(const CellSmem& S, int pos, int n, float invf) {
+  const EstSmem& E = S.est;
+  const float* tp = S.tile32 + pos;
+  float d2a = 0.f, d2b = 0.f;
+  int k = 0;
+  for (; k + 2 <= n; k += 2) {
+    const float da = tp[E.uoff[k]] - E.y0f[k];
+    const float db = tp[E.uoff[k + 1]] - E.y0f[k + 1];
+    d2a = fmaf(da, da, d2a);
+    d2b = fmaf(db, db, d2b);
+  }
+  if (k < n) {
+    const float da = tp[E.uoff[k]] - E.y0f[k];
+    d2a = fmaf(da, da, d2a);
+  }
+  return expf(-(d2a + d2b) * invf);
+}
+
 __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
                                             int C0, bool gated, float invf) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
   const int n = E.n;
-  bool adm[GH];
-  int pos[GH];
-#pragma unroll
+  // rolled over the GH entries per thread (one code copy); the window
+  // positions wait in posbuf for the compaction (0xFFFF = not admissible)
+#pragma unroll 1
   for (int h = 0; h < GH; h++) {
     const int e = e0 + h * NT + tid;
-    adm[h] = false;
-    pos[h] = 0;
-    float rw = -1.f;
+    bool adm = false;
+    int pos = 0xFFFF;
     if (e < K) {
       // ring of entry e: binary search over the ring offsets
       int lo = 1, hi = max_ring;
@@ -415,48 +436,36 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
 #pragma unroll
       for (int q = 0; q < 6; q++)
         if ((S.lostbits[wr + q] >> wc) & S.rowmask[q]) ok = false;
-      adm[h] = ok;
+      adm = ok;
+      float rw = -1.f;
       if (ok) {
-        pos[h] = wr * TS + wc;
-        rw = 0.f;
-        if (gated) {
-          // nu screening: FP32 Nadaraya-Watson distance + weight
-          const float* tp = S.tile32 + pos[h];
-          float d2a = 0.f, d2b = 0.f;
-          int k = 0;
-          for (; k + 2 <= n; k += 2) {
-            const float da = tp[E.uoff[k]] - E.y0f[k];
-            const float db = tp[E.uoff[k + 1]] - E.y0f[k + 1];
-            d2a = fmaf(da, da, d2a);
-            d2b = fmaf(db, db, d2b);
-          }
-          if (k < n) {
-            const float da = tp[E.uoff[k]] - E.y0f[k];
-            d2a = fmaf(da, da, d2a);
-          }
-          rw = expf(-(d2a + d2b) * invf);
-        }
+        pos = wr * TS + wc;
+        rw = gated ? nu_weight(S, pos, n, invf) : 0.f;
       }
       S.rbuf[e] = rw;
     }
-    const unsigned bal = __ballot_sync(FULL, adm[h]);
+    S.posbuf[h * NT + tid] = (uint16_t)pos;
+    const unsigned bal = __ballot_sync(FULL, adm);
     if (lane == 0) S.wcnt[h * NWARP + warp] = __popc(bal);
   }
   __syncthreads();
   // ordered compaction (entries are in (h, warp, lane) = expansion-map order)
   const int m0 = S.m_total;
   int tot = 0;
-#pragma unroll
+#pragma unroll 1
   for (int h = 0; h < GH; h++) {
     int base = tot;
 #pragma unroll
     for (int w = 0; w < NWARP; w++) {
-      if (w < warp) base += S.wcnt[h * NWARP + w];
-      tot += S.wcnt[h * NWARP + w];
+      const int c = S.wcnt[h * NWARP + w];
+      if (w < warp) base += c;
+      tot += c;
     }
-    const unsigned bal = __ballot_sync(FULL, adm[h]);
+    const int pos = S.posbuf[h * NT + tid];
+    const bool adm = pos != 0xFFFF;
+    const unsigned bal = __ballot_sync(FULL, adm);
     const int wpre = __popc(bal & ((1u << lane) - 1));
-    if (adm[h]) S.cand[m0 + base + wpre] = (uint16_t)pos[h];
+    if (adm) S.cand[m0 + base + wpre] = (uint16_t)pos;
   }
   __syncthreads();
   if (tid == 0) S.m_total = m0 + tot;
@@ -507,6 +516,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
       S.m_total = 0;
       S.nu = 0.0;
       S.carry = 0.0;
+      S.pref[0] = 0;
       S.cur_ring = 0;
       S.gated_stop = 0;
       S.rings_used = 0;
@@ -523,16 +533,19 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   const float invf = (float)(1.0 / (2.0 * P.sigma2 * n));
   // one screening loop (a single inlined copy of screen_chunk): ungated = the
   // whole map; gated = the first chunk, its ring-by-ring nu stop, then the
-  // rest of the map in one sweep
+  // rest of the map in one sweep.  The nu accounting (per-ring sums, one warp
+  // per ring, then the reference's sequential nu loop on thread 0) is one
+  // code copy run over entry window [0, e1) after the first chunk and, if nu
+  // has not reached T_nu, over [e1, K) after the last.
   const int e1 = min(GCH, K);
   for (int e0 = 0; e0 < K; e0 += GCH) {
     screen_chunk(S, g, e0, K, max_ring, R0, C0, gated, invf);
-    if (!gated || e0 > 0) continue;
+    if (!gated || (e0 > 0 && e0 + GCH < K)) continue;
+    const int elo = e0 == 0 ? 0 : e1, ehi = e0 == 0 ? e1 : K;
+    const int rs = e0 == 0 ? 1 : S.cur_ring;  // first ring not yet accounted (may carry a partial sum)
     if (tid == 0) S.t_g[1] = clock64();
-    // ---- first chunk, ring by ring: per-ring sums in parallel (one warp per
-    // ring), then the reference's sequential nu loop over them
-    for (int r = 1 + warp; r <= max_ring && S.ring_off[r] < e1; r += NWARP) {
-      const int lo = S.ring_off[r], hi = min(S.ring_off[r + 1], e1);
+    for (int r = rs + warp; r <= max_ring && S.ring_off[r] < ehi; r += NWARP) {
+      const int lo = max(S.ring_off[r], elo), hi = min(S.ring_off[r + 1], ehi);
       double part = 0.0;
       int c = 0;
       for (int i = lo + lane; i < hi; i += 32) {
@@ -552,16 +565,17 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     __syncthreads();
     if (tid == 0) S.t_g[2] = clock64();
     if (tid == 0) {
-      double nu = 0.0, carry = 0.0;
-      int cnt_done = 0, stop = 0, r = 1;
+      double nu = S.nu, carry = S.carry;
+      int m = S.pref[0], stop = 0, r = rs;
       for (; r <= max_ring; r++) {
-        if (S.ring_off[r] >= e1) break;  // ring starts past the first chunk
-        cnt_done += S.ringcnt[r];
-        if (S.ring_off[r + 1] > e1) {  // ring continues past the first chunk
-          carry = S.ringsum[r];
+        if (S.ring_off[r] >= ehi) break;  // ring starts past the window
+        m += S.ringcnt[r];
+        const double ring = (r == rs ? carry : 0.0) + S.ringsum[r];
+        if (S.ring_off[r + 1] > ehi) {  // ring continues past the window
+          carry = ring;
           break;
         }
-        nu += S.ringsum[r];  // nu += sum of the ring's raw weights (profiles.py:122)
+        nu += ring;  // nu += sum of the ring's raw weights (profiles.py:122)
         if (!(nu < P.t_nu) || r >= max_ring) {
           stop = 1;
           break;
@@ -571,58 +585,19 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
       S.nu = nu;
       S.carry = carry;
       S.cur_ring = r;  // stop ring, or the first ring not fully accounted
+      S.pref[0] = m;   // admissible entries of the accounted part
       if (stop) {
         S.rings_used = r;
-        S.m = cnt_done;
+        S.m = m;
       }
-      S.pref[0] = cnt_done;  // admissible entries of the accounted part
     }
     __syncthreads();
     if (tid == 0) S.t_g[3] = clock64();
     if (S.gated_stop) return;
   }
-  if (!gated) {
-    if (tid == 0) {
-      S.m = S.m_total;
-      S.rings_used = max_ring;
-    }
-    __syncthreads();
-    return;
-  }
-  // ---- the rest of the map was screened in the same loop: ring sums and the stopping ring
-  const int rs = S.cur_ring;  // first ring not yet accounted (may have a carry)
-  for (int r = rs + warp; r <= max_ring; r += NWARP) {
-    const int lo = max(S.ring_off[r], r == rs ? e1 : 0), hi = S.ring_off[r + 1];
-    double part = 0.0;
-    int c = 0;
-    for (int i = lo + lane; i < hi; i += 32) {
-      const float v = S.rbuf[i];
-      if (v >= 0.f) {
-        part += (double)v;
-        c++;
-      }
-    }
-    part = warp_sum(part);
-    c = warp_sumi(c);
-    if (lane == 0) {
-      S.ringsum[r] = part;
-      S.ringcnt[r] = c;
-    }
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double nu = S.nu;
-    int m = S.pref[0];
-    int r = rs;
-    for (; r <= max_ring; r++) {
-      const double ring = (r == rs ? S.carry : 0.0) + S.ringsum[r];
-      m += S.ringcnt[r];
-      nu += ring;
-      if (!(nu < P.t_nu) || r >= max_ring) break;
-    }
-    S.nu = nu;
-    S.rings_used = r;
-    S.m = m;
+  if (tid == 0) {  // ungated: the whole map (_forced_estimate, profiles.py:148-149)
+    S.m = S.m_total;
+    S.rings_used = max_ring;
   }
   __syncthreads();
 }
