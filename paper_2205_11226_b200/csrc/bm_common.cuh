@@ -15,7 +15,10 @@ constexpr int NT = BM_NT;        // threads per concealment CTA (2 CTAs = 2 cell
 constexpr int NWARP = NT / 32;
 constexpr int BS = 16;           // BLOCK_SIZE (image.py:18)
 constexpr int TILE = 48;         // 3x3-cell support area (framework.py:119-127)
-constexpr int TS = 52;           // tile row stride (elements); 52 = 4 mod 16 spreads 6x6 windows over banks
+#ifndef BM_TS
+#define BM_TS 53
+#endif
+constexpr int TS = BM_TS;        // tile row stride (elements); odd: fewer bank conflicts in the window gathers (A/B 52..60)
 constexpr int MAXCAND = 2048;    // >= 43*43 = 1849 window origins per support
 constexpr int MAXRING = 27;      // rings 1..26 (+ sentinel)
 constexpr int NBETA = 21;        // BETA_GRID = 2^-8 .. 2^12 (estimators.py:32)
