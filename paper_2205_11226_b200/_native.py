@@ -16,7 +16,7 @@ from .errors import DimensionMismatchError, NativeUnavailableError
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
-SOURCES = [os.path.join(PKG_DIR, "csrc", "bm_conceal.cu"), os.path.join(PKG_DIR, "csrc", "bm_aux.cu")]
+SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_conceal.cu", "bm_conceal_wide.cu", "bm_aux.cu")]
 HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh"))) + [
     os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
 ]

@@ -6,7 +6,11 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-namespace bm {
+#ifndef BM_NS
+#define BM_NS bm  // bm_conceal_wide.cu compiles the kernels again as bmw with BM_NT=512
+#endif
+
+namespace BM_NS {
 
 #ifndef BM_NT
 #define BM_NT 256
@@ -288,4 +292,4 @@ __device__ __forceinline__ double exp_w(double a, const double* __restrict__ tab
   return a <= 709.0 ? res : a * INFINITY;
 }
 
-}  // namespace bm
+}  // namespace BM_NS

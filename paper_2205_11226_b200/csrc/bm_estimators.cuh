@@ -17,7 +17,7 @@
 #include <cfloat>
 #include "bm_common.cuh"
 
-namespace bm {
+namespace BM_NS {
 
 struct TileAcc {
   const double* tile;     // smem [TILE*TS]
@@ -207,4 +207,4 @@ __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double s
   __syncthreads();
 }
 
-}  // namespace bm
+}  // namespace BM_NS

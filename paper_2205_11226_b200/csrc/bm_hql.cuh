@@ -19,7 +19,7 @@
 #include "bm_common.cuh"
 #include "bm_estimators.cuh"
 
-namespace bm {
+namespace BM_NS {
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -958,4 +958,4 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   BM_PHASE(12);
 }
 
-}  // namespace bm
+}  // namespace BM_NS
