@@ -38,8 +38,9 @@ UNIT = "blocks/s"
 # 36.8 TF/s DMMA, 36.2 DFMA (profiles/peaks_r01.txt) -> the roofline uses 36.8.
 FP64_PEAK_TFLOPS = 36.8
 FP32_PEAK_TFLOPS = 69.7  # measured FFMA peak (same run)
-LAUNCHES_PER_STEP = 11   # k_init_out, k_cell_flags, 2 x CUB scan, k_slots, 2 x k_depth,
-                         # k_sched_prep, k_sched_seed, k_conceal, k_summary (profiles/ launch list)
+LAUNCHES_PER_STEP = 12   # k_init_out, k_cell_flags, 2 x CUB scan, k_slots, 2 x k_depth, k_sched_prep,
+                         # k_sched_seed, k_conceal (256- and 512-thread builds; the one not serving
+                         # the DAG shape returns at once), k_summary (profiles/ launch list)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")  # ncu --set full dram bytes per launch
 
 WORKLOADS = {
@@ -385,7 +386,10 @@ def main():
                        "lost_cells_per_step": int(cells.item()), "patches": summ["patches"],
                        "layer_counts": summ["layer_counts"], "dag_depth": summ["max_level"],
                        "l2": "flushed (256 MiB write) between steps" if needs_flush else "inputs larger than L2",
-                       "parallelism": f"frames sharded x{world}" if scaling == "strong" else f"replicas x{world}"},
+                       "parallelism": f"frames sharded x{world}" if scaling == "strong" else f"replicas x{world}",
+                       "conceal_build": ("512-thread CTAs, 1 cell/SM (narrow DAG)"
+                                         if summ["lost_cells"] < (summ["max_level"] + 1) * 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+                                         else "256-thread CTAs, 2 cells/SM")},
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "roofline": roof,
             "cpu_baseline": cpu,
