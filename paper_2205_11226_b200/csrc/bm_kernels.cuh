@@ -44,6 +44,11 @@ struct KParams {
 };
 
 constexpr int GH = 2, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
+#ifndef BM_FIRST_GH
+#define BM_FIRST_GH 1
+#endif
+constexpr int FIRST_GH = BM_FIRST_GH;  // entries per thread of the gated first chunk
+static_assert(FIRST_GH >= 1 && FIRST_GH <= GH, "first chunk fits posbuf");
 
 struct CellSmem {
   double tile[TILE * TS];
@@ -386,15 +391,15 @@ __device__ __forceinline__ float nu_weight(const CellSmem& S, int pos, int n, fl
   return expf(-(d2a + d2b) * invf);
 }
 
-__device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int K, int max_ring, int R0,
-                                            int C0, bool gated, float invf) {
+__device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int gh, int K, int max_ring,
+                                            int R0, int C0, bool gated, float invf) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
   const int n = E.n;
-  // rolled over the GH entries per thread (one code copy); the window
+  // rolled over the gh <= GH entries per thread (one code copy); the window
   // positions wait in posbuf for the compaction (0xFFFF = not admissible)
 #pragma unroll 1
-  for (int h = 0; h < GH; h++) {
+  for (int h = 0; h < gh; h++) {
     const int e = e0 + h * NT + tid;
     bool adm = false;
     int pos = 0xFFFF;
@@ -430,7 +435,7 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
   const int m0 = S.m_total;
   int tot = 0;
 #pragma unroll 1
-  for (int h = 0; h < GH; h++) {
+  for (int h = 0; h < gh; h++) {
     int base = tot;
 #pragma unroll
     for (int w = 0; w < NWARP; w++) {
@@ -514,10 +519,12 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   // per ring, then the reference's sequential nu loop on thread 0) is one
   // code copy run over entry window [0, e1) after the first chunk and, if nu
   // has not reached T_nu, over [e1, K) after the last.
-  const int e1 = min(GCH, K);
-  for (int e0 = 0; e0 < K; e0 += GCH) {
-    screen_chunk(S, g, e0, K, max_ring, R0, C0, gated, invf);
-    if (!gated || (e0 > 0 && e0 + GCH < K)) continue;
+  const int gh1 = gated ? FIRST_GH : GH;  // gated: a smaller first chunk (IDL stops fall in rings 1..~3)
+  const int e1 = min(gh1 * NT, K);
+  for (int e0 = 0; e0 < K; e0 += (e0 == 0 ? gh1 : GH) * NT) {
+    const int gh = e0 == 0 ? gh1 : GH;
+    screen_chunk(S, g, e0, gh, K, max_ring, R0, C0, gated, invf);
+    if (!gated || (e0 > 0 && e0 + gh * NT < K)) continue;
     const int elo = e0 == 0 ? 0 : e1, ehi = e0 == 0 ? e1 : K;
     const int rs = e0 == 0 ? 1 : S.cur_ring;  // first ring not yet accounted (may carry a partial sum)
     if (tid == 0) S.t_g[1] = clock64();
