@@ -587,8 +587,6 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int r = 0; r < 4; r++) {
-        const int row = 8 * r + g;
-        const int col = 8 * c + 2 * t4;
         s0 = fma(acc[2 * r], acc[2 * r], s0);
         s1 = fma(acc[2 * r + 1], acc[2 * r + 1], s1);
       }
