@@ -66,7 +66,7 @@ typedef struct bm_params {
   double t_nu;          /* Profile.t_nu (may be +inf: sentinel) */
   double sigma2;        /* DEFAULT_SIGMA2 = 10 (estimators.py:31) */
   int32_t forced_layer; /* -1 = gated (select_and_estimate), else BM_LAYER_* (_forced_estimate) */
-  int32_t flags;        /* reserved, 0 */
+  int32_t flags;        /* BM_FLAG_* (0 = defaults) */
 } bm_params;
 
 /* One LayerDecision (profiles.py:81-95) in the reference's order
@@ -104,6 +104,12 @@ typedef struct bm_summary {
 
 /* bm_params.flags */
 #define BM_FLAG_TIME_KERNEL 1 /* time the concealment kernel with CUDA events (bm_last_kernel_ms) */
+/* Kernel build (default: by the shape of the cross-cell dependency DAG): the
+ * 256-thread CTAs (2 cells per SM) or the 512-thread CTAs (1 cell per SM).
+ * Both meet the parity bar; their FP64 reduction orders differ, so results
+ * can differ in the last bits between builds (tests, A/B). */
+#define BM_FLAG_BUILD_256 2
+#define BM_FLAG_BUILD_512 4
 
 /* ---- queries ---- */
 int bm_abi_version(void);

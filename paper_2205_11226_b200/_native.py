@@ -27,6 +27,7 @@ NVCC_FLAGS = [
 ]
 
 BM_FLAG_TIME_KERNEL = 1
+BM_FLAG_BUILD_256, BM_FLAG_BUILD_512 = 2, 4
 BM_OK, BM_ERR_ARGS, BM_ERR_LOST_LEFT, BM_ERR_CUDA, BM_ERR_WORKSPACE, BM_ERR_STATES = 0, 1, 2, 3, 4, 5
 
 

@@ -220,6 +220,7 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   P.t_nu = p->t_nu;
   P.sigma2 = p->sigma2;
   P.forced = p->forced_layer;
+  P.build = (p->flags & BM_FLAG_BUILD_512) ? 512 : ((p->flags & BM_FLAG_BUILD_256) ? 256 : 0);
   P.pixels = pixels;
   P.states = states;
   P.out_f64 = out_f64;

@@ -40,7 +40,8 @@ struct KParams {
                                  //       flop64, flop32, hql_patches, gate_candidates
   double* scratch;     // per-CTA HQL scratch
   size_t scratch_per_cta;  // doubles
-  int sms;             // SM count: CTAs >= sms step aside for narrow DAGs
+  int sms;             // SM count (narrow-DAG test)
+  int build;           // 0: by DAG shape; 256 / 512: force that kernel build
 };
 
 constexpr int GH = 2, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
@@ -869,7 +870,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
   // SM, twice the warps per cell) runs them, the other build steps aside.
   {
     const unsigned long long levels = P.counters[7] + 1;
-    const bool narrow = (unsigned long long)nslots < levels * 2ull * (unsigned long long)P.sms;
+    const bool narrow = P.build ? P.build == 512 : (unsigned long long)nslots < levels * 2ull * (unsigned long long)P.sms;
     if (narrow != (NT > 256)) return;
   }
   const long long t_cta0 = clock64();

@@ -173,13 +173,16 @@ def conceal_batch(
     out_u8=None,
     sync: bool = True,
     time_kernel: bool = False,
+    kernel_build: int | None = None,
 ) -> BatchResult:
     """Conceal B frames resident on the GPU.
 
     frames: torch.uint8 or torch.float64 [B,H,W] (cuda); states: torch.uint8
     [B,H,W] (cuda, values in {0,1,2}).  Runs asynchronously on torch's current
     stream; with sync=True the summary is read back (raising the reference's
-    errors for leftover LOST pixels / bad states).
+    errors for leftover LOST pixels / bad states).  kernel_build: None picks
+    the CTA width from the dependency DAG's shape; 256 or 512 forces one
+    (both meet the parity bar; their results can differ in the last bits).
     """
     torch = _native.require_cuda()
     if frames.dim() == 2:
@@ -204,6 +207,10 @@ def conceal_batch(
     params = make_params(b, h, w, pix_dtype, profile, sigma2, forced_layer)
     if time_kernel:
         params.flags |= _native.BM_FLAG_TIME_KERNEL
+    if kernel_build is not None:
+        if kernel_build not in (256, 512):
+            raise ValueError("kernel_build must be None, 256 or 512")
+        params.flags |= _native.BM_FLAG_BUILD_256 if kernel_build == 256 else _native.BM_FLAG_BUILD_512
     dev = frames.device
     nbytes = _WS.get(torch, params, dev, records)
     u8 = None
@@ -290,12 +297,14 @@ def conceal_image(
     sigma2: float = DEFAULT_SIGMA2,
     forced_layer: Layer | None = None,
     parallel_blocks: bool = False,
+    kernel_build: int | None = None,
 ) -> tuple[ImageBuffer, ConcealmentReport]:
     """Reconstruct every lost pixel (drop-in for blockmend.conceal_image).
 
     `parallel_blocks` is accepted for API compatibility; the GPU schedule is
     always concurrent across independent cells and bit-equivalent to the
-    serial raster order (profiles.py:285-302).
+    serial raster order (profiles.py:285-302).  kernel_build (B200-specific,
+    keyword-only): see conceal_batch.
     """
     del parallel_blocks
     pixels = img.pixels if isinstance(img, ImageBuffer) else np.asarray(img, dtype=np.float64)
@@ -307,7 +316,7 @@ def conceal_image(
     st = torch.from_numpy(np.array(states, dtype=np.uint8, copy=True)).to(dev)
     t0 = time.perf_counter()
     res = conceal_batch(px, st, profile, sigma2=sigma2, forced_layer=forced_layer, want_u8=False,
-                        want_f64=True, records=True)
+                        want_f64=True, records=True, kernel_build=kernel_build)
     out = res.recon_f64[0].cpu().numpy()
     total = time.perf_counter() - t0
     decisions = decisions_from_records(res.records, int(_native.lib().bm_device_clock_khz()))

@@ -55,13 +55,17 @@ def profile_from(t_phi, t_nu):
 # ------------------------------------------------------------ golden parity
 
 
+BUILDS = [256, 512]  # both CTA widths of the concealment kernel (bm_kernels.cuh)
+
+
+@pytest.mark.parametrize("build", BUILDS)
 @pytest.mark.parametrize("name", CASES)
-def test_golden_parity(native, name):
+def test_golden_parity(native, name, build):
     z = load(name)
     forced = int(z["forced"])
     layer = None if forced < 0 else ["BRL", "IDL", "HQL"][forced]
     out, rep = conceal_image(ImageBuffer(z["pixels"]), LossMask(z["states"]), profile_from(z["t_phi"], z["t_nu"]),
-                             forced_layer=layer)
+                             forced_layer=layer, kernel_build=build)
     recs = decisions_to_records(rep.decisions)
     res = parity.compare(z["out"], z["records"], out.pixels, recs, z["states"], float(z["t_phi"]), float(z["t_nu"]))
     assert res.ok, res.problems
@@ -92,8 +96,9 @@ CFG_CASES = [
 ]
 
 
+@pytest.mark.parametrize("build", BUILDS)
 @pytest.mark.parametrize("case", CFG_CASES, ids=[c[0] for c in CFG_CASES])
-def test_config_parity_vs_oracle(native, case):
+def test_config_parity_vs_oracle(native, case, build):
     import torch
 
     _, cfg, nf, crop, prof_name, forced = case
@@ -111,7 +116,7 @@ def test_config_parity_vs_oracle(native, case):
         px, st = make_config(cfg, frames=nf, crop=crop)
     fcode = -1 if forced is None else LAYER_CODE[forced]
     res = conceal_batch(torch.from_numpy(px).cuda(), torch.from_numpy(st).cuda(), prof, forced_layer=forced,
-                        want_f64=True, records=True)
+                        want_f64=True, records=True, kernel_build=build)
     gout = res.recon_f64.cpu().numpy()
     grec = res.records
     with ProcessPoolExecutor(max_workers=min(nf, 8)) as ex:
@@ -125,7 +130,7 @@ def test_config_parity_vs_oracle(native, case):
     o_rec = np.concatenate(o_rec)
     pr = parity.compare(o_out, o_rec, gout, grec, st, prof.t_phi, prof.t_nu)
     assert pr.ok, pr.problems[:5]
-    print(case[0], pr.summary())
+    print(case[0], build, pr.summary())
     # excluded (legitimately diverged) cells must stay rare, and even counting
     # them the u8 outputs stay within the +-1 LSB on <= 0.1% bar... up to the
     # rounding-decided beta flips of the all-HQL sentinel profile
@@ -240,6 +245,13 @@ def test_full_size_determinism_and_frame_independence(native):
     q = torch.floor(torch.clamp(a.recon_f64, 0, 255) + 0.5).to(torch.uint8)
     assert torch.equal(q, a.recon_u8)
     assert s["max_level"] >= 100  # the slice frame chains ~120 cells
+    # each forced kernel build is deterministic and keeps the same properties
+    for build in (256, 512):
+        x = conceal_batch(tp, ts, prof, want_f64=True, kernel_build=build)
+        y = conceal_batch(tp, ts, prof, want_f64=True, kernel_build=build)
+        assert torch.equal(x.recon_f64, y.recon_f64)
+        assert x.summary["layer_counts"] == y.summary["layer_counts"]
+        assert torch.equal(x.recon_u8[~lost], tp[~lost])
 
 
 def test_host_abi_matches_device_path(native):
