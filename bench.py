@@ -234,6 +234,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = each rank conceals its own batch of the config's size (default; frames are "
+                         "independent, SURVEY.md §8(e)); strong = the config's batch sharded by frame range")
     args = ap.parse_args()
 
     from paper_2205_11226_b200.parallel import dist_env, gather_frames, shard_range
@@ -256,12 +259,16 @@ def main():
     cfg, prof_name, forced = WORKLOADS[args.workload]
     prof = profile_of(prof_name)
     n_frames = CONFIGS[cfg][0]
-    if n_frames >= world:
+    if n_frames == 1:  # single-image configs: one replica per GPU
+        start, stop = 0, n_frames
+        scaling = "weak"
+        total_frames = n_frames * world
+    elif args.scaling == "strong":  # the config's batch sharded by frame range
         start, stop = shard_range(n_frames, rank, world)
         scaling = "strong"
         total_frames = n_frames
-    else:  # single-image configs: one replica per GPU
-        start, stop = 0, n_frames
+    else:  # weak: every rank conceals its own batch of the config's size (frames are independent)
+        start, stop = rank * n_frames, (rank + 1) * n_frames
         scaling = "weak"
         total_frames = n_frames * world
     px_np, st_np = make_inputs(cfg, start, stop)
@@ -275,7 +282,7 @@ def main():
     def step():
         res = conceal_batch(px, st, prof, forced_layer=forced, out_u8=out_u8, sync=False, time_kernel=True)
         if world > 1:
-            gather_frames(out_u8, n_frames, None)
+            gather_frames(out_u8, total_frames if n_frames > 1 else n_frames, None)  # result gather to rank 0
         return res
 
     for _ in range(args.warmup):
@@ -386,7 +393,8 @@ def main():
                        "lost_cells_per_step": int(cells.item()), "patches": summ["patches"],
                        "layer_counts": summ["layer_counts"], "dag_depth": summ["max_level"],
                        "l2": "flushed (256 MiB write) between steps" if needs_flush else "inputs larger than L2",
-                       "parallelism": f"frames sharded x{world}" if scaling == "strong" else f"replicas x{world}",
+                       "parallelism": (f"frames sharded x{world}" if scaling == "strong" else
+                                       f"{n_frames} frames per rank x{world}" if n_frames > 1 else f"replicas x{world}"),
                        "conceal_build": ("512-thread CTAs, 1 cell/SM (narrow DAG)"
                                          if summ["lost_cells"] < (summ["max_level"] + 1) * 2 * torch.cuda.get_device_properties(dev).multi_processor_count
                                          else "256-thread CTAs, 2 cells/SM")},
