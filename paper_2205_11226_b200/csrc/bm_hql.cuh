@@ -41,12 +41,26 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)
 #ifndef BM_CNEAR
 #define BM_CNEAR 1  // compact (rolled) per-patch code paths; 0 = the unrolled versions (A/B)
 #endif
+#ifndef BM_BETA_UNROLL
+#define BM_BETA_UNROLL 2
+#endif
+#ifndef BM_COV_UNROLL
+#define BM_COV_UNROLL 1
+#endif
+#ifndef BM_QF_UNROLL
+#define BM_QF_UNROLL 1
+#endif
 #ifndef BM_CTREE
 #define BM_CTREE 1
 #endif
 #ifndef BM_CBETA
 #define BM_CBETA 1
 #endif
+#ifndef BM_LOO_UNROLL
+#define BM_LOO_UNROLL 1
+#endif
+constexpr int kBetaUnroll = BM_BETA_UNROLL, kCovUnroll = BM_COV_UNROLL, kQfUnroll = BM_QF_UNROLL,
+              kLooUnroll = BM_LOO_UNROLL;
 constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (36 = 4 mod 16)
 #ifndef LOO_RR
 #define LOO_RR 1  // 8-row tiles of the nearest set per LOO pass over the candidates
@@ -295,7 +309,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
     };
     load_f(warp, f);
-#pragma unroll 1
+#pragma unroll kCovUnroll
     for (int s = warp; s < nks; s += NWARP) {
       load_f(s + NWARP, fn);
       int idx = 0;
@@ -567,7 +581,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       for (int kk = 0; kk < 8; kk++) o[kk] = kk < 2 * NA ? y0r[kk] - zv.at(ry[kk], bB) : 0.0;
     };
     load_v(warp, fb);
-#pragma unroll 1
+#pragma unroll kQfUnroll
     for (int c = warp; c < nct; c += NWARP) {
       load_v(c + NWARP, fbn);
       double acc[8], acb[8];  // even / odd k-steps: two independent MMA chains
@@ -647,7 +661,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       if (g == ONES_COL - 32) o[4] = 1.0;
     };
     load_b(warp, dl, fb);
-#pragma unroll 1
+#pragma unroll kBetaUnroll
     for (int s = warp; s < nks; s += NWARP) {
       load_b(s + NWARP, dln, fbn);
       double fa[3];
@@ -800,7 +814,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     for (int i = 0; i < 10 * RR; i++) acc[i] = 0.0;
     with_na(n, [&](auto NAc) {
     constexpr int NA = decltype(NAc)::value;
-#pragma unroll 1
+#pragma unroll kLooUnroll
     for (int c = warp; c < nct; c += NWARP) {
       // Gram B fragment of column tile c: (y0 - y_j)[4kk + t4] for j = 8c + g
       // (U vanishes beyond n: the padding dims' values only meet zeros)
