@@ -67,7 +67,7 @@ struct CellSmem {
   int wcnt[2 * NWARP];
   double ringsum[MAXRING + 2];
   int ringcnt[MAXRING + 2];
-  int ring_off[MAXRING + 2];
+  int ring_off[32];
   // per-patch control (written by warp 0 / thread 0, read after a barrier)
   int slot, f, gr, gc;
   unsigned long long remaining, pend;
@@ -405,13 +405,12 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
     bool adm = false;
     int pos = 0xFFFF;
     if (e < K) {
-      // ring of entry e: binary search over the ring offsets
-      int lo = 1, hi = max_ring;
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (S.ring_off[mid] <= e) lo = mid;
-        else hi = mid - 1;
-      }
+      // ring of entry e: the last ring starting at or before e (empty rings
+      // share their successor's offset), branch-free binary search over the
+      // 32 ring offsets (rings past max_ring start at K > e)
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) lo += S.ring_off[lo + step] <= e ? step : 0;
       int a, b;
       ring_entry(g, lo, e - S.ring_off[lo], a, b);
       const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
@@ -484,9 +483,9 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(FULL, inc, o);
-      if (lane >= o) inc += v;
+      inc += lane >= o ? v : 0;
     }
-    if (lane <= 27) S.ring_off[lane] = inc - cnt;  // ring_off[r] = entries of rings < r
+    S.ring_off[lane] = inc - cnt;  // ring_off[r] = entries of rings < r (K past the last ring)
     const unsigned nz = __ballot_sync(FULL, cnt > 0);
     const int mr = nz ? 31 - __clz(nz) : 0;
     const int K = __shfl_sync(FULL, inc, mr);
@@ -535,10 +534,9 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
       int c = 0;
       for (int i = lo + lane; i < hi; i += 32) {
         const float v = S.rbuf[i];
-        if (v >= 0.f) {
-          part += (double)v;
-          c++;
-        }
+        const bool ok = v >= 0.f;  // admissible
+        part += ok ? (double)v : 0.0;
+        c += ok;
       }
       part = warp_sum(part);
       c = warp_sumi(c);
