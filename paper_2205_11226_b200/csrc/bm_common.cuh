@@ -177,40 +177,28 @@ __device__ __forceinline__ int ring_count(const RingGeom& g, int r) {
   return top + nm * (lv + rv) + bot;
 }
 
-// i-th (raster-ordered) candidate patch origin of ring r.
+// i-th (raster-ordered) candidate patch origin of ring r, branch-free: ring 1
+// is the clipped 7x7 square (rows of width w); ring r > 1 is the clipped
+// square annulus at Chebyshev distance d = r + 2: its top row, then per middle
+// row the left and/or right side entries, then its bottom row.
 __device__ __forceinline__ void ring_entry(const RingGeom& g, int r, int i, int& a, int& b) {
-  if (r == 1) {
-    int a0 = max(g.A0, g.pr - 3);
-    int b0 = max(g.B0, g.pc - 3), b1 = min(g.B1, g.pc + 3);
-    int w = b1 - b0 + 1;
-    a = a0 + i / w;
-    b = b0 + i % w;
-    return;
-  }
-  const int d = r + 2;
-  int b0 = max(g.B0, g.pc - d), b1 = min(g.B1, g.pc + d);
-  int lc = b1 >= b0 ? b1 - b0 + 1 : 0;
-  int top = (g.pr - d >= g.A0 && g.pr - d <= g.A1) ? lc : 0;
-  if (i < top) {
-    a = g.pr - d;
-    b = b0 + i;
-    return;
-  }
-  i -= top;
-  int m0 = max(g.A0, g.pr - d + 1), m1 = min(g.A1, g.pr + d - 1);
-  int nm = m1 >= m0 ? m1 - m0 + 1 : 0;
-  int lv = (g.pc - d >= g.B0 && g.pc - d <= g.B1);
-  int rv = (g.pc + d >= g.B0 && g.pc + d <= g.B1);
-  int per = lv + rv;
-  if (i < nm * per) {
-    a = m0 + i / per;
-    int j = i % per;
-    b = (lv && j == 0) ? g.pc - d : g.pc + d;
-    return;
-  }
-  i -= nm * per;
-  a = g.pr + d;
-  b = b0 + i;
+  const bool first = r == 1;
+  const int d = first ? 3 : r + 2;
+  const int b0 = max(g.B0, g.pc - d), b1 = min(g.B1, g.pc + d);
+  const int lc0 = max(b1 - b0 + 1, 0), lc = max(lc0, 1);  // row width (lc >= 1 for the division)
+  // ring 1: rows of the square
+  const int q1 = i / lc;
+  const int a_sq = max(g.A0, g.pr - 3) + q1, b_sq = b0 + (i - q1 * lc);
+  // annulus
+  const int top = (g.pr - d >= g.A0 && g.pr - d <= g.A1) ? lc0 : 0;
+  const int m0 = max(g.A0, g.pr - d + 1), m1 = min(g.A1, g.pr + d - 1);
+  const int nm = max(m1 - m0 + 1, 0);
+  const int lv = (g.pc - d >= g.B0 && g.pc - d <= g.B1), rv = (g.pc + d >= g.B0 && g.pc + d <= g.B1);
+  const int per = lv + rv, sh = per >> 1;  // 2 side entries per row: i2 >> 1, i2 & 1
+  const int i2 = i - top, i3 = i2 - nm * per;
+  const int a_side = m0 + (i2 >> sh), b_side = (lv && (i2 & sh) == 0) ? g.pc - d : g.pc + d;
+  a = first ? a_sq : (i2 < 0 ? g.pr - d : (i3 < 0 ? a_side : g.pr + d));
+  b = first ? b_sq : (i2 < 0 ? b0 + i : (i3 < 0 ? b_side : b0 + i3));
 }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

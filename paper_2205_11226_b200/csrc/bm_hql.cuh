@@ -497,14 +497,12 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
         for (int i = pass & 1; i + 1 < PER; i += 2) {
           const bool sw = ev[i + 1] < ev[i] || (ev[i + 1] == ev[i] && ej[i + 1] < ej[i]);
-          if (sw) {
-            const double tv = ev[i];
-            ev[i] = ev[i + 1];
-            ev[i + 1] = tv;
-            const int tj = ej[i];
-            ej[i] = ej[i + 1];
-            ej[i + 1] = tj;
-          }
+          const double lo_v = sw ? ev[i + 1] : ev[i], hi_v = sw ? ev[i] : ev[i + 1];  // branch-free swap
+          const int lo_j = sw ? ej[i + 1] : ej[i], hi_j = sw ? ej[i] : ej[i + 1];
+          ev[i] = lo_v;
+          ev[i + 1] = hi_v;
+          ej[i] = lo_j;
+          ej[i + 1] = hi_j;
         }
       if (tid == 32) BM_DIAG_ADD(35, (clock64() - ph_t));  // sorted (diag)
       // (2) each warp merges its 32 sorted lanes into its k smallest
