@@ -50,7 +50,7 @@ namespace {
 struct Layout {
   size_t ncell;
   size_t off_slotmap, off_slot_cell, off_level, off_level2, off_height, off_bucket, off_queue, off_indeg, off_nslots,
-      off_sched, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_cub, cub_bytes, off_scratch,
+      off_sched, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_ringtab, off_cub, cub_bytes, off_scratch,
       scratch_per_cta, total;
   int grid;
 };
@@ -116,6 +116,7 @@ Layout layout(const bm_params* p) {
   L.off_cellbuf = o; o = align_up(o + nc * 256 * 8);
   L.off_reccnt = o; o = align_up(o + nc);
   L.off_counters = o; o = align_up(o + 16 * 8);
+  L.off_ringtab = o; o = align_up(o + 64 * 33 * 4);
   size_t b1 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b1, (int*)nullptr, (int*)nullptr, (int)nc);
   L.cub_bytes = b1;
@@ -237,6 +238,7 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   P.cellbuf = (double*)(ws + L.off_cellbuf);
   P.rec_count = (uint8_t*)(ws + L.off_reccnt);
   P.counters = (unsigned long long*)(ws + L.off_counters);
+  P.ringtab = (int*)(ws + L.off_ringtab);
   P.scratch = (double*)(ws + L.off_scratch);
   P.scratch_per_cta = L.scratch_per_cta;
   P.sms = sm_count();

@@ -42,6 +42,7 @@ struct KParams {
   size_t scratch_per_cta;  // doubles
   int sms;             // SM count (narrow-DAG test)
   int build;           // 0: by DAG shape; 256 / 512: force that kernel build
+  int* ringtab;        // [64][33]: interior cells' expansion-map ring offsets per patch position + max ring
 };
 
 constexpr int GH = 2, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
@@ -237,6 +238,27 @@ __device__ __forceinline__ bool cell_lost(const KParams& P, int f, int r, int c,
 // per slot: dependency count (lost earlier-raster 8-neighbours) and priority
 // bucket from the height (longest chain of dependants, k_depth<true>)
 __global__ void k_sched_prep(KParams P, const unsigned* height) {
+  if (blockIdx.x == 0 && threadIdx.x < 64) {
+    // ring offsets of an interior cell's 64 patch positions (tile coords: the
+    // support is the whole 48x48 tile, candidate origins 2..44)
+    const int p = threadIdx.x;
+    RingGeom g;
+    g.pr = BS + 2 * (p >> 3);
+    g.pc = BS + 2 * (p & 7);
+    g.A0 = 2;
+    g.A1 = TILE - 4;
+    g.B0 = 2;
+    g.B1 = TILE - 4;
+    int* t = P.ringtab + p * 33;
+    int off = 0, mr = 0;
+    for (int r = 0; r < 32; r++) {
+      t[r] = off;  // entries of rings < r
+      const int c = (r >= 1 && r <= 26) ? ring_count(g, r) : 0;
+      off += c;
+      if (c > 0) mr = r;
+    }
+    t[32] = mr;
+  }
   const int ns = *P.nslots;
   const unsigned maxh = (unsigned)P.counters[7];  // = max level = longest path
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < ns; s += gridDim.x * blockDim.x) {
@@ -478,17 +500,27 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   g.B0 = c0 + 2;
   g.B1 = c1 - 4;
   if (warp == 0) {
-    const int cnt = (lane >= 1 && lane <= 26) ? ring_count(g, lane) : 0;
-    int inc = cnt;
+    int mr, K;
+    if (r0 == br - BS && c0 == bc - BS && r1 == br + 2 * BS && c1 == bc + 2 * BS) {
+      // interior cell: the patch position's ring offsets from the table
+      // (k_sched_prep; the geometry is translation invariant)
+      const int* t = P.ringtab + (size_t)((pr_t - BS) / 2 * 8 + (pc_t - BS) / 2) * 33;
+      S.ring_off[lane] = t[lane];
+      mr = t[32];
+      K = t[31];
+    } else {
+      const int cnt = (lane >= 1 && lane <= 26) ? ring_count(g, lane) : 0;
+      int inc = cnt;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int v = __shfl_up_sync(FULL, inc, o);
-      inc += lane >= o ? v : 0;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(FULL, inc, o);
+        inc += lane >= o ? v : 0;
+      }
+      S.ring_off[lane] = inc - cnt;  // ring_off[r] = entries of rings < r (K past the last ring)
+      const unsigned nz = __ballot_sync(FULL, cnt > 0);
+      mr = nz ? 31 - __clz(nz) : 0;
+      K = __shfl_sync(FULL, inc, mr);
     }
-    S.ring_off[lane] = inc - cnt;  // ring_off[r] = entries of rings < r (K past the last ring)
-    const unsigned nz = __ballot_sync(FULL, cnt > 0);
-    const int mr = nz ? 31 - __clz(nz) : 0;
-    const int K = __shfl_sync(FULL, inc, mr);
     __syncwarp();
     if (lane == 0) {
       S.max_ring = mr;
