@@ -850,14 +850,14 @@ __device__ void pick_and_extract(CellSmem& S) {
     E.y0f[idx] = S.tile32[o];
     E.uoff[idx] = (int16_t)(ctx_r(lane) * TS + ctx_c(lane));
   }
-  // row masks of used window positions (usable context + patch cells): one
-  // redux.or per window row
-  const unsigned mybit = usable ? 1u << ctx_c(lane) : 0u;
-#pragma unroll
-  for (int q = 0; q < 6; q++) {
-    unsigned rm = __reduce_or_sync(FULL, ctx_r(lane) == q ? mybit : 0u);
-    if (q == 2 || q == 3) rm |= (1u << 2) | (1u << 3);
-    if (lane == q) S.rowmask[q] = rm;
+  // row masks of used window positions (usable context + patch cells) from
+  // the usable ballot: context offsets 0-5 / 6-11 are window rows 0 / 1
+  // (cols 0-5), 12-15 / 16-19 rows 2 / 3 (cols 0, 1, 4, 5; the patch cells 2,
+  // 3 are always used), 20-25 / 26-31 rows 4 / 5 (CONTEXT_OFFSETS, framework.py:33-36)
+  if (lane < 6) {
+    const int sh = lane < 2 ? 6 * lane : (lane < 4 ? 12 + 4 * (lane - 2) : 20 + 6 * (lane - 4));
+    const unsigned b = bal >> sh;
+    S.rowmask[lane] = (lane == 2 || lane == 3) ? ((b & 3u) | ((b & 0xCu) << 2) | 0xCu) : (b & 0x3Fu);
   }
   if (lane < 4) E.uoff[n + lane] = (int16_t)((2 + (lane >> 1)) * TS + 2 + (lane & 1));
   // flatness (profiles.py:98-102): exact max / min of y0 by redux on
