@@ -57,6 +57,8 @@ struct CellSmem {
   float tile32[TILE * TS];
   uint64_t lostbits[TILE];
   uint64_t availbits[TILE];
+  int pkey[64];  // schedule key per patch (patch_key), maintained across write-backs
+  int wb_lost;   // LOST pixels of the patch just written back
   uint8_t st[TILE * TS];
   uint16_t cand[MAXCAND];
   uint16_t posbuf[GH * NT];  // screen_chunk: window positions of the chunk's entries
@@ -779,13 +781,21 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
   // write back (profiles.py:229-235) + record
   if (tid < 4) {
     const int o = (pr_t + (tid >> 1)) * TS + pc_t + (tid & 1);
-    if (S.st[o] == ST_LO) {
+    const bool lost = S.st[o] == ST_LO;
+    if (lost) {
       S.tile[o] = E.vals[tid];
       S.tile32[o] = (float)E.vals[tid];
       S.st[o] = ST_RE;
     }
+    const unsigned wl = __ballot_sync(0xFu, lost);
+    if (tid == 0) S.wb_lost = __popc(wl);
   }
   __syncthreads();
+  if (tid >= 32 && tid < 40) {  // the 8 neighbouring patches gain usable context
+    const int k = tid - 32, d = k < 4 ? k : k + 1;  // 3x3 neighbourhood minus the centre
+    const int qr = (p >> 3) + d / 3 - 1, qc = (p & 7) + d % 3 - 1;
+    if (qr >= 0 && qr < 8 && qc >= 0 && qc < 8) S.pkey[qr * 8 + qc] += S.wb_lost << 7;
+  }
   if (tid < 2) {
     const int r = pr_t + tid;
     uint64_t b = S.lostbits[r];
@@ -811,30 +821,38 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
 
 // pick_next_patch (framework.py:243-250) + extract_target (framework.py:151-168)
 // by warp 0.  Returns via S.pick / S.skip.
+// Schedule key of patch p (patch_scores, framework.py:230-240): AVAILABLE
+// count, then usable (not LOST) count over the 32 context offsets, then raster
+// order; from the row bitmaps (6 window rows of 6 bits, patch cells masked out;
+// out-of-image positions are LOST).  Computed for the 64 patches at cell start;
+// a write-back only raises the usable counts of the 8 neighbouring patches
+// (every neighbour's window covers the whole written patch; AVAILABLE pixels
+// never change), so the keys are maintained incrementally (commit of a patch).
+__device__ __forceinline__ int patch_key(const CellSmem& S, int p) {
+  const int pr = patch_r(p), pc = patch_c(p);
+  int av = 0, us = 0;
+#pragma unroll
+  for (int q = 0; q < 6; q++) {
+    const unsigned m6 = (q == 2 || q == 3) ? 0x33u : 0x3Fu;
+    const unsigned lb = (unsigned)(S.lostbits[pr - 2 + q] >> (pc - 2)) & m6;
+    const unsigned ab = (unsigned)(S.availbits[pr - 2 + q] >> (pc - 2)) & m6;
+    us += __popc(m6 & ~lb);
+    av += __popc(ab);
+  }
+  return (av << 13) | (us << 7) | (63 - p);
+}
+
 __device__ void pick_and_extract(CellSmem& S) {
   const int lane = threadIdx.x & 31;
   EstSmem& E = S.est;
   const unsigned long long pend = S.pend;
+  // pick_next_patch (framework.py:243-250): the pending patch with the largest
+  // schedule key (patch_key, maintained as patches are written back)
   int best_key = -1;
 #pragma unroll
   for (int h = 0; h < 2; h++) {
     const int p = lane + 32 * h;
-    if ((pend >> p) & 1ull) {
-      // patch_scores (framework.py:230-240) from the row bitmaps: 6 window rows
-      // of 6 bits, patch cells masked out; out-of-image positions are LOST
-      const int pr = patch_r(p), pc = patch_c(p);
-      int av = 0, us = 0;
-#pragma unroll
-      for (int q = 0; q < 6; q++) {
-        const unsigned m6 = (q == 2 || q == 3) ? 0x33u : 0x3Fu;
-        const unsigned lb = (unsigned)(S.lostbits[pr - 2 + q] >> (pc - 2)) & m6;
-        const unsigned ab = (unsigned)(S.availbits[pr - 2 + q] >> (pc - 2)) & m6;
-        us += __popc(m6 & ~lb);
-        av += __popc(ab);
-      }
-      const int key = (av << 13) | (us << 7) | (63 - p);
-      best_key = max(best_key, key);
-    }
+    if ((pend >> p) & 1ull) best_key = max(best_key, S.pkey[p]);
   }
   best_key = __reduce_max_sync(FULL, (unsigned)(best_key + 1)) - 1;
   const int p = 63 - (best_key & 127);
@@ -933,6 +951,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
         const bool l = S.st[o] == ST_LO || S.st[o + 1] == ST_LO || S.st[o + TS] == ST_LO || S.st[o + TS + 1] == ST_LO;
         const unsigned b = __ballot_sync(FULL, l);
         bits |= (unsigned long long)b << (32 * h);
+        S.pkey[p] = patch_key(S, p);
       }
       if (tid == 0) {
         S.remaining = bits;
