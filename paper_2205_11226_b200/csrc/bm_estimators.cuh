@@ -128,7 +128,7 @@ __device__ __forceinline__ void brl_values(EstSmem& S) {
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
 template <class Acc>
 __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf,
-                                                 bool want_raw) {
+                                                 bool want_raw, bool final_sync = true) {
   const int n = S.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const double c = 2.0 * sigma2 * n;
   double emax = -INFINITY;
@@ -204,7 +204,7 @@ __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double s
       }
     }
   }
-  __syncthreads();
+  if (final_sync) __syncthreads();
 }
 
 }  // namespace BM_NS

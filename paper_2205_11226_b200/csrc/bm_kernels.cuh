@@ -77,7 +77,7 @@ struct CellSmem {
   int deferred[64];
   int ndef, progressed, nrec;
   int pick, skip, gated_stop;
-  int m, m_total, rings_used, max_ring, K, cur_ring;
+  int m, rings_used, max_ring, K, cur_ring;
   double nu, carry, phi;
   unsigned rowmask[6];
   long long t_start, t_mark, t_pick, t_gather, t_g[4];
@@ -417,7 +417,7 @@ __device__ __forceinline__ float nu_weight(const CellSmem& S, int pos, int n, fl
 }
 
 __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int gh, int K, int max_ring,
-                                            int R0, int C0, bool gated, float invf) {
+                                            int R0, int C0, bool gated, float invf, int m0, bool sync_end) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
   const int n = E.n;
@@ -456,7 +456,6 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
   }
   __syncthreads();
   // ordered compaction (entries are in (h, warp, lane) = expansion-map order)
-  const int m0 = S.m_total;
   int tot = 0;
 #pragma unroll 1
   for (int h = 0; h < gh; h++) {
@@ -473,8 +472,9 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
     const int wpre = __popc(bal & ((1u << lane) - 1));
     if (adm) S.cand[m0 + base + wpre] = (uint16_t)pos;
   }
-  __syncthreads();
-  if (tid == 0) S.m_total = m0 + tot;
+  // (wcnt / posbuf are reused by the next chunk; when the nu accounting
+  // follows, its barrier comes first)
+  if (sync_end) __syncthreads();
   return tot;
 }
 
@@ -529,7 +529,6 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
       S.K = mr ? K : 0;
       S.ring_off[mr + 1] = S.K;
       S.m = 0;
-      S.m_total = 0;
       S.nu = 0.0;
       S.carry = 0.0;
       S.pref[0] = 0;
@@ -555,10 +554,12 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   // has not reached T_nu, over [e1, K) after the last.
   const int gh1 = gated ? FIRST_GH : GH;  // gated: a smaller first chunk (IDL stops fall in rings 1..~3)
   const int e1 = min(gh1 * NT, K);
+  int mtot = 0;  // admissible candidates gathered so far (the same in every thread)
   for (int e0 = 0; e0 < K; e0 += (e0 == 0 ? gh1 : GH) * NT) {
     const int gh = e0 == 0 ? gh1 : GH;
-    screen_chunk(S, g, e0, gh, K, max_ring, R0, C0, gated, invf);
-    if (!gated || (e0 > 0 && e0 + gh * NT < K)) continue;
+    const bool acct = gated && (e0 == 0 || e0 + gh * NT >= K);  // nu accounting after this chunk
+    mtot += screen_chunk(S, g, e0, gh, K, max_ring, R0, C0, gated, invf, mtot, !acct);
+    if (!acct) continue;
     const int elo = e0 == 0 ? 0 : e1, ehi = e0 == 0 ? e1 : K;
     const int rs = e0 == 0 ? 1 : S.cur_ring;  // first ring not yet accounted (may carry a partial sum)
     if (tid == 0) S.t_g[1] = clock64();
@@ -613,7 +614,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     if (S.gated_stop) return;
   }
   if (tid == 0) {  // ungated: the whole map (_forced_estimate, profiles.py:148-149)
-    S.m = S.m_total;
+    S.m = mtot;
     S.rings_used = max_ring;
   }
   __syncthreads();
@@ -713,7 +714,9 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     }
     const bool run_idl = !done && m >= 1;  // (mode 0 has m >= 1: nu > 0)
     if (run_idl) {
-      idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1, mode != 0);
+      // gated IDL (mode 0): only thread 0 reads the outcome, and the branch
+      // ends with a CTA barrier -> no barrier after the estimate's last step
+      idl_estimate_dev(acc, m, P.sigma2, E, S.hql.R1, mode != 0, mode != 0);
       if (tid == 0) S.cnt[4] += idl_flops(m, E.n);
     }
     if (mode == 0) {
