@@ -66,15 +66,17 @@ def _gen_frame(args):
     return px[0], st[0]
 
 
-def make_inputs(cfg: int, start: int, stop: int):
-    """Frames [start, stop) of config `cfg` (host numpy), generated in parallel."""
+def make_inputs(cfg: int, start: int, stop: int, ranks: int = 1):
+    """Frames [start, stop) of config `cfg` (host numpy), generated in parallel
+    (the host cores shared by the `ranks` processes of this node)."""
     from multiprocessing import Pool
 
     idx = list(range(start, stop))
-    if len(idx) <= 2:
+    procs = max(1, min(len(idx), (os.cpu_count() or 1) // max(1, ranks)))
+    if len(idx) <= 2 or procs == 1:
         res = [_gen_frame((cfg, f)) for f in idx]
     else:
-        with Pool(min(len(idx), os.cpu_count() or 1)) as pool:
+        with Pool(procs) as pool:
             res = pool.map(_gen_frame, [(cfg, f) for f in idx])
     return np.stack([r[0] for r in res]), np.stack([r[1] for r in res])
 
@@ -271,7 +273,7 @@ def main():
         start, stop = rank * n_frames, (rank + 1) * n_frames
         scaling = "weak"
         total_frames = n_frames * world
-    px_np, st_np = make_inputs(cfg, start, stop)
+    px_np, st_np = make_inputs(cfg, start, stop, world)
     px = torch.from_numpy(px_np).to(dev)
     st = torch.from_numpy(st_np).to(dev)
     out_u8 = torch.empty_like(px)
