@@ -17,7 +17,7 @@ from .errors import DimensionMismatchError, NativeUnavailableError
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
 SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_conceal.cu", "bm_conceal_wide.cu", "bm_aux.cu")]
-HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh"))) + [
+HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh")) + glob.glob(os.path.join(PKG_DIR, "csrc", "*.h"))) + [
     os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
 ]
 NVCC_FLAGS = [

@@ -21,6 +21,7 @@
 #include <cstring>
 
 #include "../../include/blockmend_b200.h"
+#include "bm_host.h"
 
 namespace bm_aux {
 
@@ -223,15 +224,7 @@ __global__ void k_mask_paint(const uint8_t* lost, int B, int H, int W, int bs, i
   }
 }
 
-int sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
-  }
-  return n;
-}
+int sms() { return bm_host::sm_count(); }
 
 int status(cudaError_t e) { return e == cudaSuccess ? BM_OK : BM_ERR_CUDA; }
 
@@ -269,8 +262,8 @@ int bm_ssim_batch(const void* ref, const void* test, int pixel_dtype, int frames
   if (pixel_dtype != BM_PIX_U8 && pixel_dtype != BM_PIX_F64) return BM_ERR_ARGS;
   if (height < SW || width < SW) return BM_ERR_ARGS;  // metrics.py:96-97
   cudaStream_t st = (cudaStream_t)stream_;
-  static bool init = false;
-  if (!init) {
+  bm_host::DevState& D = bm_host::dev_state();
+  if (!D.ssim_init.load()) {
     // normalised Gaussian taps (metrics.py:_gaussian_kernel_1d), computed in FP64 on the host
     double g[SW], s = 0.0;
     for (int i = 0; i < SW; i++) {
@@ -283,7 +276,7 @@ int bm_ssim_batch(const void* ref, const void* test, int pixel_dtype, int frames
     if (cudaFuncSetAttribute(k_ssim_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SsimSmem)) !=
         cudaSuccess)
       return BM_ERR_CUDA;
-    init = true;
+    D.ssim_init = true;
   }
   const int vh = height - 2 * HALF, vw = width - 2 * HALF;
   const int tiles_y = (vh + TO - 1) / TO, tiles_x = (vw + TO - 1) / TO, ntile = tiles_x * tiles_y;
@@ -318,8 +311,12 @@ int bm_gen_masks(int kind, int frames, int height, int width, int block_size, in
   if (!in_smem && (e = cudaMallocAsync((void**)&scratch, (size_t)frames * total * 4, st)) != cudaSuccess)
     return status(e);
   const int smem = in_smem ? total * 4 : 0;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_mask_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  if (smem > 48 * 1024 && !bm_host::dev_state().mask_attr.load()) {
+    if ((e = cudaFuncSetAttribute(k_mask_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024)) !=
+        cudaSuccess)
+      return status(e);
+    bm_host::dev_state().mask_attr = true;
+  }
   if (rows > 0 && cols > 0)
     k_mask_blocks<<<frames, NT, smem, st>>>(kind, rows, cols, count, seeds, scratch, lost);
   else

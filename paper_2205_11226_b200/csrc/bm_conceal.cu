@@ -31,6 +31,7 @@
 #include <cstring>
 #include <mutex>
 
+#include "bm_host.h"
 #include "bm_kernels.cuh"
 
 namespace bm_wide {  // bm_conceal_wide.cu: the 512-thread build of k_conceal
@@ -55,38 +56,29 @@ struct Layout {
   int grid;
 };
 
-int g_sms = 0;
-int sm_count() {
-  if (!g_sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) g_sms = 148;
-  }
-  return g_sms;
-}
+int sm_count() { return bm_host::sm_count(); }
 
 size_t align_up(size_t v) { return (v + 255) & ~(size_t)255; }
 
-bool g_attr_set = false;
-bool g_attr_w = false;  // the 512-thread build's shared-memory attribute
-
-// resident concealment CTAs per SM (persistent grid = SMs x this)
+// resident concealment CTAs per SM (persistent grid = SMs x this), per device
 int cells_per_sm() {
-  static int occ = 0;
-  if (!occ) {
+  bm_host::DevState& D = bm_host::dev_state();
+  if (!D.occ) {
     const int smem = (int)sizeof(CellSmem);
-    if (!g_attr_set) {
+    if (!D.attr.load()) {
       if (cudaFuncSetAttribute(k_conceal, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess)
-        g_attr_set = true;
+        D.attr = true;
     }
+    int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_conceal, NT, smem) != cudaSuccess || occ < 1) occ = 1;
     // dev/diagnostic override (tools/): fewer resident cells per SM
     if (const char* e = getenv("BM_CELLS_PER_SM")) {
       const int v = atoi(e);
       if (v >= 1 && v < occ) occ = v;
     }
+    D.occ = occ;
   }
-  return occ;
+  return D.occ;
 }
 
 bool params_ok(const bm_params* p) {
@@ -254,8 +246,10 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   const int sms = sm_count();
   // dense outputs first (non-lost cells keep their input values)
   if (out_f64 || out_u8) k_init_out<<<sms * 4, 256, 0, stream>>>(P);
+  // lost flags per cell, LOST pixels outside the block grid and the state
+  // range check: always, also for frames smaller than one cell (ncell = 0)
+  k_cell_flags<<<sms * 4, 256, 0, stream>>>(P, flags);
   if (nc > 0) {
-    k_cell_flags<<<sms * 4, 256, 0, stream>>>(P, flags);
     size_t cb = L.cub_bytes;
     if ((e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cb, flags, excl, nc, stream)) != cudaSuccess)
       return cuda_status(e);
@@ -268,14 +262,15 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
     k_sched_prep<<<sms, 256, 0, stream>>>(P, height);
     k_sched_seed<<<sms, 256, 0, stream>>>(P);
     const size_t smem = sizeof(CellSmem), smem_w = bm_wide::cell_smem_bytes();
-    if (!g_attr_set) {
+    bm_host::DevState& D = bm_host::dev_state();
+    if (!D.attr.load()) {
       if ((e = cudaFuncSetAttribute(k_conceal, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
         return cuda_status(e);
-      g_attr_set = true;
+      D.attr = true;
     }
-    if (!g_attr_w) {
+    if (!D.attr_w.load()) {
       if ((e = bm_wide::set_smem(smem_w)) != cudaSuccess) return cuda_status(e);
-      g_attr_w = true;
+      D.attr_w = true;
     }
     const bool timed = (p->flags & BM_FLAG_TIME_KERNEL) != 0;
     const int slot_ev = g_nev < NEV ? g_nev : NEV - 1;
@@ -344,12 +339,12 @@ int bm_estimate_batch(int32_t layer, int32_t count, int32_t max_m, double sigma2
   if ((e = cudaMallocAsync((void**)&scratch, (size_t)count * per * 8, stream)) != cudaSuccess) return cuda_status(e);
   EstBatchArgs A{layer, count, max_m, sigma2, n_y, m, y0, x, y, out_values, out_info, scratch};
   const size_t smem = sizeof(EstBatchSmem);
-  static bool attr = false;
-  if (!attr) {
+  bm_host::DevState& D = bm_host::dev_state();
+  if (!D.est_attr.load()) {
     if ((e = cudaFuncSetAttribute(k_estimate_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
         cudaSuccess)
       return cuda_status(e);
-    attr = true;
+    D.est_attr = true;
   }
   k_estimate_batch<<<count, NT, smem, stream>>>(A);
   if ((e = cudaGetLastError()) != cudaSuccess) return cuda_status(e);
@@ -385,14 +380,15 @@ int bm_conceal_host(const bm_params* p, const void* pixels, const uint8_t* state
   const size_t wsb = bm_workspace_bytes(p);
   const size_t rec_cap = out_records ? (size_t)bm_max_records(p) : 0;
   if (npix != C.npix || pixbytes != C.pixbytes || wsb > C.ws_bytes || rec_cap > C.rec_cap) {
+    cudaStreamSynchronize(C.stream);
     cudaFree(C.d_pix); cudaFree(C.d_ws); cudaFree(C.d_st); cudaFree(C.d_u8); cudaFree(C.d_f64);
     cudaFree(C.d_rec); cudaFree(C.d_rec2); cudaFree(C.d_sum);
+    cudaStreamDestroy(C.stream);
     C = HostCache{};
     if ((e = cudaStreamCreateWithFlags(&C.stream, cudaStreamNonBlocking)) != cudaSuccess) return cuda_status(e);
     if ((e = cudaMalloc(&C.d_pix, pixbytes)) != cudaSuccess) return cuda_status(e);
     if ((e = cudaMalloc((void**)&C.d_st, npix)) != cudaSuccess) return cuda_status(e);
     if ((e = cudaMalloc((void**)&C.d_u8, npix)) != cudaSuccess) return cuda_status(e);
-    if ((e = cudaMalloc((void**)&C.d_f64, npix * 8)) != cudaSuccess) return cuda_status(e);
     if ((e = cudaMalloc(&C.d_ws, wsb)) != cudaSuccess) return cuda_status(e);
     if ((e = cudaMalloc((void**)&C.d_sum, sizeof(bm_summary))) != cudaSuccess) return cuda_status(e);
     if (rec_cap) {
@@ -404,6 +400,8 @@ int bm_conceal_host(const bm_params* p, const void* pixels, const uint8_t* state
     C.ws_bytes = wsb;
     C.rec_cap = rec_cap;
   }
+  // the FP64 output buffer only when FP64 output is requested (8 B/pixel)
+  if (out_f64 && !C.d_f64 && (e = cudaMalloc((void**)&C.d_f64, npix * 8)) != cudaSuccess) return cuda_status(e);
   if ((e = cudaMemcpyAsync(C.d_pix, pixels, pixbytes, cudaMemcpyHostToDevice, C.stream)) != cudaSuccess)
     return cuda_status(e);
   if ((e = cudaMemcpyAsync(C.d_st, states, npix, cudaMemcpyHostToDevice, C.stream)) != cudaSuccess)

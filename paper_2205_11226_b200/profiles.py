@@ -121,31 +121,26 @@ class BatchResult:
     records: np.ndarray | None  # host RECORD_DTYPE array in the reference's decision order
 
 
-class _Workspace:
-    def __init__(self):
-        self.key = None
-        self.buf = None
-        self.summary = None
-        self.rec = None
-        self.rec2 = None
+def _workspace(torch, params, device, want_records):
+    """Per-call device buffers (workspace, summary, record slots).
 
-    def get(self, torch, params, device, want_records):
-        lib = _native.lib()
-        nbytes = int(lib.bm_workspace_bytes(params))
-        nrec = int(lib.bm_max_records(params)) if want_records else 0
-        key = (device, nbytes)
-        if self.key != key:
-            self.buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
-            self.summary = torch.zeros(_native.SUMMARY_BYTES, dtype=torch.uint8, device=device)
-            self.key = key
-            self.rec = self.rec2 = None
-        if nrec and (self.rec is None or self.rec.numel() < nrec * RECORD_DTYPE.itemsize):
-            self.rec = torch.empty(nrec * RECORD_DTYPE.itemsize, dtype=torch.uint8, device=device)
-            self.rec2 = torch.empty_like(self.rec)
-        return nbytes
-
-
-_WS = _Workspace()
+    Allocated from torch's caching allocator on the call's stream, so repeated
+    calls reuse the same memory without a module-global buffer: concurrent
+    calls (threads, streams, devices) never share a workspace, which keeps
+    conceal_batch / conceal_image reentrant like the reference's pure
+    function.
+    """
+    lib = _native.lib()
+    nbytes = int(lib.bm_workspace_bytes(params))
+    buf = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+    summary = torch.zeros(_native.SUMMARY_BYTES, dtype=torch.uint8, device=device)
+    rec = rec2 = None
+    if want_records:
+        # at least one record slot: frames smaller than one 16x16 cell have none
+        nrec = max(1, int(lib.bm_max_records(params)))
+        rec = torch.empty(nrec * RECORD_DTYPE.itemsize, dtype=torch.uint8, device=device)
+        rec2 = torch.empty_like(rec)
+    return nbytes, buf, summary, rec, rec2
 
 
 def make_params(frames, height, width, pixel_dtype, profile, sigma2, forced_layer) -> _native.Params:
@@ -212,52 +207,52 @@ def conceal_batch(
             raise ValueError("kernel_build must be None, 256 or 512")
         params.flags |= _native.BM_FLAG_BUILD_256 if kernel_build == 256 else _native.BM_FLAG_BUILD_512
     dev = frames.device
-    nbytes = _WS.get(torch, params, dev, records)
-    u8 = None
-    if want_u8:
-        u8 = out_u8 if out_u8 is not None else torch.empty((b, h, w), dtype=torch.uint8, device=dev)
-    f64 = torch.empty((b, h, w), dtype=torch.float64, device=dev) if want_f64 else None
-    stream = torch.cuda.current_stream(dev).cuda_stream
-    lib = _native.lib()
-    _native.check(
-        lib.bm_conceal(
-            params, frames.data_ptr(), states.data_ptr(), f64.data_ptr() if f64 is not None else None,
-            u8.data_ptr() if u8 is not None else None, _WS.rec.data_ptr() if records else None,
-            _WS.summary.data_ptr(), _WS.buf.data_ptr(), nbytes, stream,
-        )
-    )
-    summary = None
-    recs = None
-    if sync or records:
-        raw = _WS.summary.cpu().numpy().tobytes()
-        s = _native.Summary.from_buffer_copy(raw)
-        summary = {
-            "lost_cells": int(s.lost_cells),
-            "patches": int(s.patches),
-            "layer_counts": {"BRL": int(s.layer_counts[0]), "IDL": int(s.layer_counts[1]), "HQL": int(s.layer_counts[2])},
-            "deferred_fills": int(s.deferred_fills),
-            "lost_left": int(s.lost_left),
-            "max_level": int(s.max_level),
-            "bad_states": int(s.bad_states),
-            "flop64": int(s.flop64),
-            "flop32": int(s.flop32),
-            "hql_patches": int(s.hql_patches),
-            "gate_candidates": int(s.gate_candidates),
-        }
-        if s.bad_states:
-            _native.check(_native.BM_ERR_STATES)
-        if s.lost_left:
-            _native.check(_native.BM_ERR_LOST_LEFT)
-        if records:
-            import ctypes
-
-            cnt = ctypes.c_int64(0)
-            _native.check(
-                lib.bm_compact_records(params, _WS.rec.data_ptr(), _WS.buf.data_ptr(), _WS.rec2.data_ptr(),
-                                       ctypes.byref(cnt), stream)
+    with torch.cuda.device(dev):  # the C ABI works on the current device
+        nbytes, ws, summ_buf, rec, rec2 = _workspace(torch, params, dev, records)
+        u8 = None
+        if want_u8:
+            u8 = out_u8 if out_u8 is not None else torch.empty((b, h, w), dtype=torch.uint8, device=dev)
+        f64 = torch.empty((b, h, w), dtype=torch.float64, device=dev) if want_f64 else None
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        lib = _native.lib()
+        _native.check(
+            lib.bm_conceal(
+                params, frames.data_ptr(), states.data_ptr(), f64.data_ptr() if f64 is not None else None,
+                u8.data_ptr() if u8 is not None else None, rec.data_ptr() if records else None,
+                summ_buf.data_ptr(), ws.data_ptr(), nbytes, stream,
             )
-            n = int(cnt.value)
-            recs = _WS.rec2[: n * RECORD_DTYPE.itemsize].cpu().numpy().view(RECORD_DTYPE).copy()
+        )
+        summary = None
+        recs = None
+        if sync or records:
+            raw = summ_buf.cpu().numpy().tobytes()
+            s = _native.Summary.from_buffer_copy(raw)
+            summary = {
+                "lost_cells": int(s.lost_cells),
+                "patches": int(s.patches),
+                "layer_counts": {"BRL": int(s.layer_counts[0]), "IDL": int(s.layer_counts[1]),
+                                 "HQL": int(s.layer_counts[2])},
+                "deferred_fills": int(s.deferred_fills),
+                "lost_left": int(s.lost_left),
+                "max_level": int(s.max_level),
+                "bad_states": int(s.bad_states),
+                "flop64": int(s.flop64),
+                "flop32": int(s.flop32),
+                "hql_patches": int(s.hql_patches),
+                "gate_candidates": int(s.gate_candidates),
+            }
+            if s.bad_states:
+                _native.check(_native.BM_ERR_STATES)
+            if s.lost_left:
+                _native.check(_native.BM_ERR_LOST_LEFT)
+            if records:
+                import ctypes
+
+                cnt = ctypes.c_int64(0)
+                _native.check(lib.bm_compact_records(params, rec.data_ptr(), ws.data_ptr(), rec2.data_ptr(),
+                                                     ctypes.byref(cnt), stream))
+                n = int(cnt.value)
+                recs = rec2[: n * RECORD_DTYPE.itemsize].cpu().numpy().view(RECORD_DTYPE).copy()
     return BatchResult(u8, f64, summary, recs)
 
 

@@ -221,6 +221,51 @@ def test_lost_left_and_bad_states(native):
         conceal_batch(torch.zeros((1, 32, 32), dtype=torch.uint8, device="cuda"), bad, Profile.named("express"))
 
 
+@pytest.mark.parametrize("shape", [(10, 10), (12, 40), (40, 15), (1, 1)])
+def test_frames_smaller_than_one_cell(native, shape):
+    """No full 16x16 cell: the reference returns the image unchanged when no
+    pixel is LOST and raises AssertionError otherwise (profiles.py:305); bad
+    state values raise ValueError (image.py:69-70) - also without cells."""
+    import torch
+
+    img = ImageBuffer(np.arange(shape[0] * shape[1], dtype=np.float64).reshape(shape) % 251)
+    out, rep = conceal_image(img, LossMask(np.zeros(shape, np.uint8)), Profile.named("efficient"))
+    assert np.array_equal(out.pixels, img.pixels) and rep.patches == 0 and rep.decisions == []
+    st = np.zeros(shape, np.uint8)
+    st[shape[0] // 2, shape[1] // 2] = PixelState.LOST
+    with pytest.raises(AssertionError):
+        conceal_image(img, LossMask(st), Profile.named("efficient"))
+    bad = torch.zeros((1,) + shape, dtype=torch.uint8, device="cuda")
+    bad[0, 0, 0] = 9
+    with pytest.raises(ValueError):
+        conceal_batch(torch.zeros((1,) + shape, dtype=torch.uint8, device="cuda"), bad, Profile.named("express"))
+
+
+def test_concurrent_calls_are_independent(native):
+    """conceal_image is a pure function, safe to call from several threads at
+    once: per-call workspaces, no shared result buffers."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    cases = []
+    for seed, rate in ((3, 0.3), (4, 0.2), (5, 0.4), (6, 0.25)):
+        px, st = make_config(2, frames=1, crop=(96, 128), first=seed)
+        cases.append((ImageBuffer(px[0].astype(np.float64)), LossMask(st[0])))
+    prof = Profile.named("efficient")
+    serial = [conceal_image(img, m, prof) for img, m in cases]
+
+    def run(i):
+        img, m = cases[i % len(cases)]
+        return i % len(cases), conceal_image(img, m, prof)
+
+    with ThreadPoolExecutor(8) as ex:
+        results = list(ex.map(run, range(16)))
+    for i, (out, rep) in results:
+        s_out, s_rep = serial[i]
+        assert np.array_equal(out.pixels, s_out.pixels)
+        assert [(d.patch_origin, d.layer, d.beta) for d in rep.decisions] == \
+            [(d.patch_origin, d.layer, d.beta) for d in s_rep.decisions]
+
+
 # --------------------------------------------- full-size properties
 
 
@@ -236,9 +281,13 @@ def test_full_size_determinism_and_frame_independence(native):
     assert a.summary["lost_left"] == 0 and a.summary["lost_cells"] > 0
     s = a.summary
     assert s["patches"] == sum(s["layer_counts"].values()) + s["deferred_fills"]
-    # frame 4 alone == frame 4 inside the batch (frames are independent)
-    c = conceal_batch(tp[4:5], ts[4:5], prof, want_f64=True)
-    assert torch.equal(c.recon_f64[0], a.recon_f64[4])
+    # frame 4 alone == frame 4 inside the batch (frames are independent) for a
+    # fixed kernel build (the default build is chosen from the batch's DAG
+    # shape, and the two builds' FP64 reduction orders differ in the last bits)
+    for build in (256, 512):
+        full = conceal_batch(tp, ts, prof, want_f64=True, kernel_build=build)
+        c = conceal_batch(tp[4:5], ts[4:5], prof, want_f64=True, kernel_build=build)
+        assert torch.equal(c.recon_f64[0], full.recon_f64[4])
     # non-lost pixels untouched; u8 is the half-up quantization of f64
     lost = ts == PixelState.LOST
     assert torch.equal(a.recon_u8[~lost], tp[~lost])
