@@ -144,32 +144,39 @@ def _oracle_crop(args):
     return cells, time.perf_counter() - t0
 
 
+def host_cores() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
 def cpu_jobs(workload: str, crop: int = 384):
     """Bounded CPU sample of the workload: one crop x crop tile (multiple of 16)
-    per host core, from the workload's own frames; built outside any timing."""
+    per host core from the workload's own frames, at crop positions spread
+    over the whole frame (a seeded draw per core, not only the corner where
+    the support areas are clipped); built outside any timing."""
     cfg, prof_name, forced = WORKLOADS[workload]
     prof = profile_of(prof_name)
     forced_code = -1 if forced is None else {"BRL": 0, "IDL": 1, "HQL": 2}[forced]
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    cores = host_cores()
     nb = CONFIGS[cfg][0]
     px_all, st_all = make_inputs(cfg, 0, min(nb, cores))
     h, w = px_all.shape[1:]
     crop = min(crop, h // 16 * 16, w // 16 * 16)
-    gy, gx = max(h // crop, 1), max(w // crop, 1)
+    gy, gx = max((h - crop) // 16 + 1, 1), max((w - crop) // 16 + 1, 1)  # 16-aligned crop origins
+    rng = np.random.default_rng(20260)
     jobs = []
     for i in range(cores):
         f = i % px_all.shape[0]
-        k = i // px_all.shape[0]
-        y0 = (k % gy) * crop
-        x0 = ((k // gy) % gx) * crop
+        y0 = int(rng.integers(0, gy)) * 16
+        x0 = int(rng.integers(0, gx)) * 16
         jobs.append((px_all[f, y0 : y0 + crop, x0 : x0 + crop], st_all[f, y0 : y0 + crop, x0 : x0 + crop],
                      prof.t_phi, prof.t_nu, forced_code))
     return jobs, cores, crop
 
 
-def cpu_baseline(workload: str, jobs=None):
+def cpu_baseline(workload: str, jobs=None, pool=None):
     """Oracle (plain-C FP64 port of the reference path) on all host cores over
-    the bounded sample of cpu_jobs (one process per core)."""
+    the bounded sample of cpu_jobs (one process per core).  `pool`: a
+    multiprocessing Pool created once by the caller (outside the timing)."""
     from multiprocessing import Pool
 
     from oracle import oracle
@@ -178,10 +185,17 @@ def cpu_baseline(workload: str, jobs=None):
     if jobs is None:
         jobs = cpu_jobs(workload)
     jobs, cores, crop = jobs
-    t0 = time.perf_counter()
-    with Pool(cores) as pool:
-        res = pool.map(_oracle_crop, jobs)
-    wall = time.perf_counter() - t0
+    own = pool is None
+    if own:
+        pool = Pool(cores)
+    try:
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_crop, jobs, chunksize=1)
+        wall = time.perf_counter() - t0
+    finally:
+        if own:
+            pool.close()
+            pool.join()
     cells = sum(r[0] for r in res)
     return {
         "value": cells / wall,
@@ -190,31 +204,39 @@ def cpu_baseline(workload: str, jobs=None):
         "unit": UNIT,
         "cores": cores,
         "kind": "port",
-        "sample": f"{cores} crops {crop}x{crop} of {workload} frames ({cells} lost cells), one process per core, "
-                  f"plain-C FP64 oracle, {wall:.1f}s wall",
+        "sample": f"{cores} crops {crop}x{crop} at seeded positions over {workload} frames ({cells} lost cells), "
+                  f"one process per core, plain-C FP64 oracle, {wall:.1f}s wall",
     }
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the CPU reference path (oracle port) on the host cores;
+    rank 0 alone works under torchrun, the other ranks exit without work."""
     if rank != 0:
         return
+    from multiprocessing import Pool
+
+    from oracle import oracle
+
+    oracle.lib()
     jobs = cpu_jobs(args.workload)
     times = []
     cells = []
     last = None
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        last = cpu_baseline(args.workload, jobs)
-        if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
-            cells.append(last["cells"])
+    with Pool(jobs[1]) as pool:  # created once, outside the timed steps
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            last = cpu_baseline(args.workload, jobs, pool)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+                cells.append(last["cells"])
     value = float(np.sum(cells)) / float(np.sum(times))  # lost cells over the timed steps / their wall time
     last = dict(last, value=value)
     cfg, prof_name, forced = WORKLOADS[args.workload]
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": default_scaling(args, cfg), "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "impl": "reference",
         "config": {"workload": args.workload, "profile": prof_name, "forced_layer": forced,
                    "baseline_config": CONFIGS[cfg][:3]},
@@ -224,7 +246,158 @@ def run_reference(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------- launcher
+
+
+def free_port() -> int:
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-exec under torchrun with N
+    ranks (one process per GPU, rendezvous on 127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, BM_BENCH_RELAUNCHED="1")
+    return subprocess.call(cmd, env=env)
+
+
+def default_scaling(args, cfg: int) -> str:
+    """Batch configs shard the config's own batch (strong); single-image
+    configs run one replica per GPU (weak)."""
+    if CONFIGS[cfg][0] == 1:
+        return "weak"
+    return "strong" if args.scaling == "auto" else args.scaling
+
+
+def blocks8_lost(st_np) -> int:
+    """Lost 8x8 blocks (SURVEY.md §8(d) secondary unit of cfg 4)."""
+    b, h, w = st_np.shape
+    g = (st_np[:, : h // 8 * 8, : w // 8 * 8] == 1).reshape(b, h // 8, 8, w // 8, 8)
+    return int(g.any(axis=(2, 4)).sum())
+
+
 # ----------------------------------------------------------------------- ours
+
+
+class Timer:
+    """Device time of one step: CUDA events on the launching stream (GPU), or
+    the host clock for the CPU stub (--stub, launcher tests)."""
+
+    def __init__(self, torch, cuda: bool):
+        self.torch, self.cuda = torch, cuda
+        if cuda:
+            self.e0 = torch.cuda.Event(enable_timing=True)
+            self.e1 = torch.cuda.Event(enable_timing=True)
+
+    def start(self):
+        if self.cuda:
+            self.e0.record()
+        else:
+            self.t0 = time.perf_counter()
+
+    def stop(self) -> float:
+        if self.cuda:
+            self.e1.record()
+            self.e1.synchronize()
+            return self.e0.elapsed_time(self.e1)
+        return 1e3 * (time.perf_counter() - self.t0)
+
+
+def measure(args, ctx, frame_range, n_total):
+    """W warm-up + K timed steps over frames [start, stop) of the workload on
+    this rank, each step = concealment of the rank's frames + the result
+    gather to rank 0.  Returns the per-rank timing and counts."""
+    torch, dev, world, cuda = ctx["torch"], ctx["dev"], ctx["world"], ctx["cuda"]
+    from paper_2205_11226_b200.parallel import FrameGather
+
+    cfg, prof_name, forced = WORKLOADS[args.workload]
+    start, stop = frame_range
+    if args.stub:  # launcher test: tiny frames, the step is a host copy
+        px_np = np.zeros((stop - start, 32, 48), np.uint8)
+        for i in range(stop - start):
+            px_np[i] = (start + i if CONFIGS[cfg][0] > 1 else ctx["rank"]) % 251
+        st_np = np.zeros_like(px_np)
+    else:
+        px_np, st_np = make_inputs(cfg, start, stop, world)
+    px = torch.from_numpy(px_np).to(dev)
+    st = torch.from_numpy(st_np).to(dev)
+    gather = FrameGather(n_total, px.shape[1], px.shape[2], torch.uint8, dev)
+    assert gather.local.shape[0] == px.shape[0]
+    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev) if cuda else None
+    needs_flush = cuda and px.numel() * 2 < 2 * 126 * 1024 * 1024
+    prof = profile_of(prof_name)
+    if not args.stub:
+        from paper_2205_11226_b200 import _native
+        from paper_2205_11226_b200.profiles import conceal_batch
+
+    def step():
+        if args.stub:
+            gather.local.copy_(px)
+        else:
+            conceal_batch(px, st, prof, forced_layer=forced, out_u8=gather.local, sync=False, time_kernel=True)
+        gather.gather()  # the result gather to rank 0 (the path's only collective)
+
+    for _ in range(args.warmup):
+        step()
+    if cuda:
+        torch.cuda.synchronize()
+        _native.kernel_times_reset()
+    if world > 1:
+        ctx["dist"].barrier()
+    if cuda:
+        torch.cuda.synchronize()
+    timer = Timer(torch, cuda)
+    step_ms = []
+    with ClockSampler(ctx["local_rank"]) if cuda else _Null() as clk:
+        for _ in range(args.steps):
+            if needs_flush:
+                flush_l2(torch, l2)
+            timer.start()
+            step()
+            step_ms.append(timer.stop())
+    if cuda:
+        torch.cuda.synchronize()
+    if world > 1:
+        ctx["dist"].barrier()
+    kms = _native.kernel_times_ms() if cuda else []
+    if args.stub:
+        summ = {"lost_cells": int(px.shape[0]), "patches": 0, "layer_counts": {}, "max_level": 0,
+                "flop64": 0, "flop32": 0}
+    else:  # counts / algorithmic work of one (deterministic) step
+        summ = conceal_batch(px, st, prof, forced_layer=forced, out_u8=gather.local, sync=True).summary
+    frames = gather.frames()
+    if frames is not None and ctx["rank"] == 0:
+        assert frames.shape[0] == n_total
+        if args.stub and stop - start < n_total:  # every rank's frames arrived in order at rank 0
+            want = torch.arange(start if world == 1 else 0, (start if world == 1 else 0) + n_total) % 251
+            assert torch.equal(frames[:, 0, 0].to(torch.int64), want), "result gather out of order"
+    return {"px_np": px_np, "st_np": st_np, "step_ms": step_ms, "kms": kms, "summ": summ,
+            "clocks": clk.summary() if cuda else None, "px": px}
+
+
+class _Null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def reduce_max_sum(ctx, local_ms: float, cells: float):
+    torch = ctx["torch"]
+    t = torch.tensor([local_ms], dtype=torch.float64, device=ctx["dev"])
+    c = torch.tensor([cells], dtype=torch.float64, device=ctx["dev"])
+    if ctx["world"] > 1:
+        ctx["dist"].all_reduce(t, op=ctx["dist"].ReduceOp.MAX)
+        ctx["dist"].all_reduce(c, op=ctx["dist"].ReduceOp.SUM)
+    return float(t.item()), float(c.item())
 
 
 def main():
@@ -236,97 +409,79 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = each rank conceals its own batch of the config's size (default; frames are "
-                         "independent, SURVEY.md §8(e)); strong = the config's batch sharded by frame range")
+    ap.add_argument("--scaling", default="auto", choices=["auto", "weak", "strong"],
+                    help="auto (default): batch configs shard the config's own batch by frame range over the N "
+                         "ranks (strong scaling) and also report weak scaling (every rank its own batch of the "
+                         "config's size) in `secondary`; single-image configs run one replica per GPU")
+    ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU launcher test (gloo, no GPU)
     args = ap.parse_args()
 
-    from paper_2205_11226_b200.parallel import dist_env, gather_frames, shard_range
+    from paper_2205_11226_b200.parallel import dist_env, shard_range
 
     rank, world, local_rank = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} runs under a world of {world} ranks")
 
     import torch
     import torch.distributed as dist
 
-    from paper_2205_11226_b200 import _native
-    from paper_2205_11226_b200.profiles import conceal_batch, make_params
-
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    cuda = not args.stub
+    if cuda:
+        torch.cuda.set_device(local_rank)
+        dev = torch.device("cuda", local_rank)
+    else:
+        dev = torch.device("cpu")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if cuda:
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+        assert dist.get_world_size() == args.gpus
+    ctx = {"torch": torch, "dist": dist, "dev": dev, "world": world, "rank": rank, "local_rank": local_rank,
+           "cuda": cuda}
     cfg, prof_name, forced = WORKLOADS[args.workload]
     prof = profile_of(prof_name)
     n_frames = CONFIGS[cfg][0]
+    scaling = default_scaling(args, cfg)
     if n_frames == 1:  # single-image configs: one replica per GPU
-        start, stop = 0, n_frames
-        scaling = "weak"
-        total_frames = n_frames * world
-    elif args.scaling == "strong":  # the config's batch sharded by frame range
-        start, stop = shard_range(n_frames, rank, world)
-        scaling = "strong"
-        total_frames = n_frames
+        rng_main, n_total = (0, 1), 1
+    elif scaling == "strong":  # the config's own batch sharded by frame range
+        rng_main, n_total = shard_range(n_frames, rank, world), n_frames
     else:  # weak: every rank conceals its own batch of the config's size (frames are independent)
-        start, stop = rank * n_frames, (rank + 1) * n_frames
-        scaling = "weak"
-        total_frames = n_frames * world
-    px_np, st_np = make_inputs(cfg, start, stop, world)
-    px = torch.from_numpy(px_np).to(dev)
-    st = torch.from_numpy(st_np).to(dev)
-    out_u8 = torch.empty_like(px)
-    l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
-    in_bytes = px.numel() * 2
-    needs_flush = in_bytes < 2 * 126 * 1024 * 1024
-
-    def step():
-        res = conceal_batch(px, st, prof, forced_layer=forced, out_u8=out_u8, sync=False, time_kernel=True)
-        if world > 1:
-            gather_frames(out_u8, total_frames if n_frames > 1 else n_frames, None)  # result gather to rank 0
-        return res
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    _native.kernel_times_reset()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    step_ms = []
-    with ClockSampler(local_rank) as clk:
-        for _ in range(args.steps):
-            if needs_flush:
-                flush_l2(torch, l2)
-            ev0.record()
-            step()
-            ev1.record()
-            ev1.synchronize()
-            step_ms.append(ev0.elapsed_time(ev1))
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    kms = _native.kernel_times_ms()
-    # summary of one (deterministic) step for counts / algorithmic work
-    res = conceal_batch(px, st, prof, forced_layer=forced, out_u8=out_u8, sync=True)
-    summ = res.summary
-    local_ms = float(np.sum(step_ms))
-    t = torch.tensor([local_ms], dtype=torch.float64, device=dev)
-    cells = torch.tensor([float(summ["lost_cells"])], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.all_reduce(cells, op=dist.ReduceOp.SUM)
-    total_ms = float(t.item())
+        rng_main, n_total = (rank * n_frames, (rank + 1) * n_frames), n_frames * world
+    # replicas gather one frame per rank; batch configs gather the frames
+    m = measure(args, ctx, rng_main, n_total if n_frames > 1 else world)
+    total_ms, cells = reduce_max_sum(ctx, float(np.sum(m["step_ms"])), float(m["summ"]["lost_cells"]))
     ms_per_step = total_ms / args.steps
-    value = float(cells.item()) / (ms_per_step / 1e3)
+    value = cells / (ms_per_step / 1e3)
+    summ, px_np, st_np, px = m["summ"], m["px_np"], m["st_np"], m["px"]
+    blocks8 = None
+    if cfg == 4 and not args.stub:
+        _, b8 = reduce_max_sum(ctx, 0.0, float(blocks8_lost(st_np)))
+        blocks8 = b8 / (ms_per_step / 1e3)
+
+    # weak scaling as the secondary line of a strong N > 1 run
+    secondary = {}
+    if world > 1 and n_frames > 1 and scaling == "strong" and args.scaling == "auto":
+        wk = measure(args, ctx, (rank * n_frames, (rank + 1) * n_frames), n_frames * world)
+        w_ms, w_cells = reduce_max_sum(ctx, float(np.sum(wk["step_ms"])), float(wk["summ"]["lost_cells"]))
+        secondary["weak"] = {"value": w_cells / (w_ms / args.steps / 1e3), "unit": UNIT,
+                             "ms_per_step": w_ms / args.steps, "frames_per_rank": n_frames,
+                             "frames": n_frames * world}
+        del wk
 
     # ---- e2e through the C ABI with host buffers (pinned), every step H2D + D2H
     e2e = None
-    if not args.no_e2e:
+    if cuda and not args.no_e2e:
         import ctypes
+
+        from paper_2205_11226_b200 import _native
+        from paper_2205_11226_b200.profiles import make_params
 
         lib = _native.lib()
         params = make_params(px.shape[0], px.shape[1], px.shape[2], 0, prof, 10.0, forced)
@@ -343,72 +498,83 @@ def main():
         for _ in range(args.steps):
             _native.check(lib.bm_conceal_host(params, h_px.data_ptr(), h_st.data_ptr(), None, h_out.data_ptr(),
                                               None, None, ctypes.byref(summ_h)))
-        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(cells.item()) * args.steps / float(e2e_s.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(h_px.numel() + h_st.numel()), "d2h_bytes_per_step": int(h_out.numel())
-               + ctypes.sizeof(_native.Summary)}
+        e2e_ms, _ = reduce_max_sum(ctx, 1e3 * (time.perf_counter() - t0), 0.0)
+        e2e = {"value": cells * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(h_px.numel() + h_st.numel()),
+               "d2h_bytes_per_step": int(h_out.numel()) + ctypes.sizeof(_native.Summary),
+               "path": "bm_conceal_host (C ABI, host buffers), per rank"}
 
     if rank == 0:
+        kms = m["kms"]
         kmean = float(np.mean(kms)) if kms else None
-        flop64 = summ["flop64"]
-        flop32 = summ["flop32"]
         roof = None
         if kmean:
-            a64 = flop64 / (kmean * 1e-3) / 1e12
-            a32 = flop32 / (kmean * 1e-3) / 1e12
-            traffic = None
-            try:
-                with open(TRAFFIC_FILE) as fh:
-                    tr = json.load(fh).get(args.workload)
-                if tr and tr.get("frames") == int(px.shape[0]):  # same launch size as profiled
-                    traffic = tr["dram_bytes_per_launch"]
-            except (OSError, ValueError):
-                pass
-            roof = {
-                "bound": "fp64", "achieved": a64, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": a64 / FP64_PEAK_TFLOPS, "traffic": traffic,
-                "traffic_unit": "bytes per k_conceal launch (dram__bytes_read.sum + dram__bytes_write.sum, "
-                                "ncu --set full, profiles/ncu_traffic.json)",
-                "algorithmic_bytes_per_launch": int(px.numel() * 2 + out_u8.numel()),
-                "kernel": "bm::k_conceal", "kernel_ms": kmean, "kernel_share_of_step": kmean / ms_per_step,
-                "flop64_per_launch": flop64, "flop32_per_launch": flop32,
-                "fp32_gate": {"achieved": a32, "peak": FP32_PEAK_TFLOPS, "frac": a32 / FP32_PEAK_TFLOPS},
-                "composite_frac": a64 / FP64_PEAK_TFLOPS + a32 / FP32_PEAK_TFLOPS,
-                "peak_source": "measured on this pool's B200: DMMA m8n8k4 f64 36.8 TF/s (DFMA 36.2, same FP64 "
-                               "hardware), FFMA 69.7 TF/s (tools/peakbench.cu, tools/pipebench.cu; "
-                               "MEASURED_PEAKS.json has HBM and bf16 only)",
-            }
+            roof = roofline(args, summ, kmean, ms_per_step, px)
         cpu = None
-        if not args.no_cpu_baseline and world == 1:
+        if cuda and not args.no_cpu_baseline and world == 1:
             try:
                 cpu = cpu_baseline(args.workload)
             except Exception as exc:  # reported, not fatal
                 cpu = {"error": repr(exc)}
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count if cuda else 148
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": scaling,
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic" if not args.stub else "stub",
             "config": {"workload": args.workload, "profile": prof_name, "forced_layer": forced,
-                       "frames": total_frames, "height": int(px.shape[1]), "width": int(px.shape[2]),
-                       "lost_cells_per_step": int(cells.item()), "patches": summ["patches"],
+                       "frames": n_total, "height": int(px.shape[1]), "width": int(px.shape[2]),
+                       "lost_cells_per_step": int(cells), "patches": summ["patches"],
                        "layer_counts": summ["layer_counts"], "dag_depth": summ["max_level"],
-                       "l2": "flushed (256 MiB write) between steps" if needs_flush else "inputs larger than L2",
-                       "parallelism": (f"frames sharded x{world}" if scaling == "strong" else
+                       "l2": "flushed (256 MiB write) between steps" if px.numel() * 2 < 2 * 126 * 1024 * 1024
+                             else "inputs larger than L2",
+                       "parallelism": (f"frames sharded x{world} (strong)" if scaling == "strong" and world > 1 else
                                        f"{n_frames} frames per rank x{world}" if n_frames > 1 else f"replicas x{world}"),
+                       "result_gather": "dist.gather of the u8 frames to rank 0 (NCCL), preallocated buffers",
                        "conceal_build": ("512-thread CTAs, 1 cell/SM (narrow DAG)"
-                                         if summ["lost_cells"] < (summ["max_level"] + 1) * 2 * torch.cuda.get_device_properties(dev).multi_processor_count
+                                         if summ["lost_cells"] < (summ["max_level"] + 1) * 2 * sms
                                          else "256-thread CTAs, 2 cells/SM")},
-            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps if cuda else 0,
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "clocks": clk.summary(),
+            "clocks": m["clocks"],
         }
+        if blocks8 is not None:
+            secondary["lost_8x8_blocks_per_s"] = blocks8
+        if secondary:
+            out["secondary"] = secondary
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline(args, summ, kmean, ms_per_step, px):
+    flop64 = summ["flop64"]
+    flop32 = summ["flop32"]
+    a64 = flop64 / (kmean * 1e-3) / 1e12
+    a32 = flop32 / (kmean * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(TRAFFIC_FILE) as fh:
+            tr = json.load(fh).get(args.workload)
+        if tr and tr.get("frames") == int(px.shape[0]):  # same launch size as profiled
+            traffic = tr["dram_bytes_per_launch"]
+    except (OSError, ValueError):
+        pass
+    return {
+        "bound": "fp64", "achieved": a64, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+        "frac": a64 / FP64_PEAK_TFLOPS, "traffic": traffic,
+        "traffic_unit": "bytes per k_conceal launch (dram__bytes_read.sum + dram__bytes_write.sum, "
+                        "ncu --set full, profiles/ncu_traffic.json)",
+        "algorithmic_bytes_per_launch": int(px.numel() * 3),
+        "kernel": "bm::k_conceal", "kernel_ms": kmean, "kernel_share_of_step": kmean / ms_per_step,
+        "flop64_per_launch": flop64, "flop32_per_launch": flop32,
+        "fp32_gate": {"achieved": a32, "peak": FP32_PEAK_TFLOPS, "frac": a32 / FP32_PEAK_TFLOPS},
+        "composite_frac": a64 / FP64_PEAK_TFLOPS + a32 / FP32_PEAK_TFLOPS,
+        "peak_source": "measured on this pool's B200: DMMA m8n8k4 f64 36.8 TF/s (DFMA 36.2, same FP64 "
+                       "hardware), FFMA 69.7 TF/s (tools/peakbench.cu, tools/pipebench.cu; "
+                       "MEASURED_PEAKS.json has HBM and bf16 only)",
+    }
 
 
 if __name__ == "__main__":

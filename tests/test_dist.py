@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2205_11226_b200.parallel import gather_frames, shard_range
+from paper_2205_11226_b200.parallel import FrameGather, gather_frames, shard_range
 
 
 def _free_port():
@@ -32,6 +32,19 @@ def _worker(rank, world, port, n_total, ret):
         ret.put([int(full[f, 0, 0]) for f in range(n_total)] + [tuple(full.shape)])
     else:
         assert full is None
+    # repeated gathers through one preallocated FrameGather (the bench's timed step)
+    g = FrameGather(n_total, 4, 6, torch.uint8, torch.device("cpu"))
+    assert g.local.shape[0] == stop - start
+    send_ptr = g.send.data_ptr()
+    for it in range(3):
+        g.local.copy_(local + it)
+        g.gather()
+        assert g.send.data_ptr() == send_ptr  # no per-step allocation
+        res = g.frames()
+        if rank == 0:
+            assert [int(res[f, 0, 0]) for f in range(n_total)] == [f + it for f in range(n_total)]
+        else:
+            assert res is None
     dist.destroy_process_group()
 
 
