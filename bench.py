@@ -527,7 +527,7 @@ def main():
                        "layer_counts": summ["layer_counts"], "dag_depth": summ["max_level"],
                        "l2": "flushed (256 MiB write) between steps" if px.numel() * 2 < 2 * 126 * 1024 * 1024
                              else "inputs larger than L2",
-                       "parallelism": (f"frames sharded x{world} (strong)" if scaling == "strong" and world > 1 else
+                       "parallelism": (f"frames sharded x{world} (strong)" if scaling == "strong" else
                                        f"{n_frames} frames per rank x{world}" if n_frames > 1 else f"replicas x{world}"),
                        "result_gather": "dist.gather of the u8 frames to rank 0 (NCCL), preallocated buffers",
                        "conceal_build": ("512-thread CTAs, 1 cell/SM (narrow DAG)"

@@ -218,6 +218,76 @@ int bm_estimate_batch(int32_t layer, int32_t count, int32_t max_m, double sigma2
                       const double* x, const double* y, double* out_values,
                       bm_patch_record* out_info, void* stream);
 
+/* ---- the per-patch library API (blockmend/__init__.py:17-58) ------------
+ * Device entry points behind the reference's framework / estimator / profile
+ * functions that a library user (or the reference's own unit tests) calls
+ * one patch at a time.  Device pointers, one working image [H,W] (FP64
+ * pixels, u8 PixelState states), asynchronous on `stream`. */
+
+/* select_and_estimate (profiles.py:105-133) — or _forced_estimate
+ * (profiles.py:141-171) when p->forced_layer >= 0 — for `count` independent
+ * patches of the working image (p->frames = 1, p->pixel_dtype = BM_PIX_F64):
+ * the fused kernel's patch step (gate, ring gather with the nu loop, IDL /
+ * HQL with the ladder), no write-back.  The caller's TargetContext per patch:
+ * origins [count][2], layouts [count] (bit k = CONTEXT_OFFSETS[k] usable,
+ * framework.py:33-36), y0 [count][32] (layout order).  Outputs: values
+ * [count][4] and one bm_patch_record per patch (layer, phi, nu, rings,
+ * m_candidates, beta, alpha, fallback). */
+int bm_select_and_estimate(const bm_params* p, const double* pixels, const uint8_t* states, int32_t count,
+                           const int32_t* origins, const uint32_t* layouts, const double* y0,
+                           double* out_values, bm_patch_record* out_records, void* stream);
+
+/* extract_target (framework.py:151-168) for `count` patch origins:
+ * out_layouts [count], out_n_y [count], out_y0 [count][32]. */
+int bm_extract_targets(int height, int width, const double* pixels, const uint8_t* states, int32_t count,
+                       const int32_t* origins, uint32_t* out_layouts, int32_t* out_n_y, double* out_y0,
+                       void* stream);
+
+/* _collect (framework.py:171-183), the masked gather under gather_candidates
+ * / expand_support (framework.py:186-207): request q screens the window
+ * origins [offsets[q], offsets[q] + counts[q]) of `origins` ([.][2]) with
+ * layout layouts[q] and writes its admissible candidates, in list order, at
+ * the same offsets of out_x [.][4] and out_y [.][32]; out_m[q] = their count. */
+int bm_collect(int height, int width, const double* pixels, const uint8_t* states, int32_t requests,
+               const int32_t* origins, const int32_t* offsets, const int32_t* counts, const uint32_t* layouts,
+               double* out_x, double* out_y, int32_t* out_m, void* stream);
+
+/* patch_scores (framework.py:230-240): AVAILABLE / usable context counts. */
+int bm_patch_scores(int height, int width, const uint8_t* states, int32_t count, const int32_t* origins,
+                    int32_t* out_avail, int32_t* out_usable, void* stream);
+
+/* build_schedule (framework.py:253-274) for `count` blocks (block ids
+ * [count][2]): out_n [count] jobs, out_origins [count][64][2],
+ * out_reliability [count][64], in filling order. */
+int bm_build_schedule(int height, int width, const uint8_t* states, int32_t count, const int32_t* blocks,
+                      int32_t* out_n, int32_t* out_origins, int32_t* out_reliability, void* stream);
+
+/* build_expansion_map (framework.py:130-148) for `count` patch origins:
+ * out_k [count] entries, out_origins [count][2048][2] window origins and
+ * out_rings [count][2048], sorted by (ring, row, col). */
+int bm_expansion_maps(int height, int width, int32_t count, const int32_t* origins, int32_t* out_k,
+                      int32_t* out_origins, int32_t* out_rings, void* stream);
+
+/* Estimator stages (estimators.py:105-245) on `count` dense instances (the
+ * bm_estimate_batch layout: n_y, m, y0 [count][32], x [count][max_m][4],
+ * y [count][max_m][32]).  cov [count][BM_COV_DOUBLES] = c_xx [4][4],
+ * c_xy [4][32], c_yy [32][32] (ridge included), ridge: written by
+ * BM_STAGE_COVARIANCE, read by the stages that take a CovarianceBlocks.
+ * out_status[i]: 0 ok, 2 C_YY not positive definite (LinAlgError). */
+#define BM_STAGE_COVARIANCE 0     /* sample_covariance -> cov */
+#define BM_STAGE_KERNEL_WEIGHTS 1 /* kernel_weights(beta[i], cov) -> out_w [count][max_m], scalars[0] raw_sum */
+#define BM_STAGE_OPTIMIZE_BETA 2  /* optimize_beta(cov) -> scalars[0] beta, [1] its eps */
+#define BM_STAGE_OPTIMIZE_ALPHA 3 /* optimize_alpha(beta[i], cov) -> scalars[0] alpha */
+#define BM_STAGE_IDL_WEIGHTS 4    /* idl_weights(sigma2) -> out_w, scalars[0] raw_sum; out_mat[i][j][0] (if
+                                     not NULL) = raw_idl_weights r_j */
+#define BM_STAGE_PREDICT 5        /* predict_xy(w = out_w as input) -> scalars[0..3] x~, [4..4+n) y~ */
+#define BM_STAGE_SOLVE 6          /* CovarianceBlocks.solve_yy: out_mat [count][max_m][32] = C_YY^-1 y_j */
+#define BM_COV_DOUBLES (16 + 128 + 1024 + 1)
+int bm_estimator_stages(int32_t stage, int32_t count, int32_t max_m, double sigma2, const int32_t* n_y,
+                        const int32_t* m, const double* y0, const double* x, const double* y, const double* beta,
+                        double* cov, double* out_w, double* out_mat, double* out_scalars, int32_t* out_status,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

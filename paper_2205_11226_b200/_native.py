@@ -16,7 +16,7 @@ from .errors import DimensionMismatchError, NativeUnavailableError
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
-SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_conceal.cu", "bm_conceal_wide.cu", "bm_aux.cu")]
+SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_conceal.cu", "bm_conceal_wide.cu", "bm_aux.cu", "bm_api.cu")]
 HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh")) + glob.glob(os.path.join(PKG_DIR, "csrc", "*.h"))) + [
     os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
 ]
@@ -67,6 +67,8 @@ EXPORTS = [
     "bm_kernel_times_ms", "bm_kernel_times_reset", "bm_debug_phase_cycles",
     "bm_conceal", "bm_compact_records", "bm_conceal_host", "bm_estimate_batch",
     "bm_sqdiff_batch", "bm_ssim_batch", "bm_gen_masks",
+    "bm_select_and_estimate", "bm_extract_targets", "bm_collect", "bm_patch_scores", "bm_build_schedule",
+    "bm_expansion_maps", "bm_estimator_stages",
 ]
 
 
@@ -136,6 +138,20 @@ def lib():
     L.bm_ssim_batch.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp]
     L.bm_gen_masks.restype = ctypes.c_int
     L.bm_gen_masks.argtypes = [i32, i32, i32, i32, i32, i32, vp, vp, vp]
+    L.bm_select_and_estimate.restype = ctypes.c_int
+    L.bm_select_and_estimate.argtypes = [ctypes.POINTER(Params), vp, vp, i32, vp, vp, vp, vp, vp, vp]
+    L.bm_extract_targets.restype = ctypes.c_int
+    L.bm_extract_targets.argtypes = [i32, i32, vp, vp, i32, vp, vp, vp, vp, vp]
+    L.bm_collect.restype = ctypes.c_int
+    L.bm_collect.argtypes = [i32, i32, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.bm_patch_scores.restype = ctypes.c_int
+    L.bm_patch_scores.argtypes = [i32, i32, vp, i32, vp, vp, vp, vp]
+    L.bm_build_schedule.restype = ctypes.c_int
+    L.bm_build_schedule.argtypes = [i32, i32, vp, i32, vp, vp, vp, vp, vp]
+    L.bm_expansion_maps.restype = ctypes.c_int
+    L.bm_expansion_maps.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp]
+    L.bm_estimator_stages.restype = ctypes.c_int
+    L.bm_estimator_stages.argtypes = [i32, i32, i32, ctypes.c_double, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     _lib = L
     return L
 

@@ -352,6 +352,41 @@ int bm_estimate_batch(int32_t layer, int32_t count, int32_t max_m, double sigma2
   return BM_OK;
 }
 
+int bm_select_and_estimate(const bm_params* p, const double* pixels, const uint8_t* states, int32_t count,
+                           const int32_t* origins, const uint32_t* layouts, const double* y0,
+                           double* out_values, bm_patch_record* out_records, void* stream_) {
+  if (!params_ok(p) || p->frames != 1 || p->pixel_dtype != BM_PIX_F64 || !pixels || !states || count < 0)
+    return BM_ERR_ARGS;
+  if (count == 0) return BM_OK;
+  if (!origins || !layouts || !y0 || !out_values || !out_records) return BM_ERR_ARGS;
+  cudaStream_t stream = (cudaStream_t)stream_;
+  KParams P;
+  memset(&P, 0, sizeof(P));
+  P.B = 1;
+  P.H = p->height;
+  P.W = p->width;
+  P.GR = p->height / BS;
+  P.GC = p->width / BS;
+  P.pix_f64 = 1;
+  P.t_phi = p->t_phi;
+  P.t_nu = p->t_nu;
+  P.sigma2 = p->sigma2;
+  P.forced = p->forced_layer;
+  P.pixels = pixels;
+  P.states = states;  // slotmap / ringtab / records stay null: values straight from the working image
+  SelectArgs A{count, origins, layouts, y0, out_values, out_records};
+  const size_t smem = sizeof(CellSmem);
+  cudaError_t e;
+  bm_host::DevState& D = bm_host::dev_state();
+  if (!D.select_attr.load()) {
+    if ((e = cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return cuda_status(e);
+    D.select_attr = true;
+  }
+  k_select<<<count, NT, smem, stream>>>(P, A);
+  return cuda_status(cudaGetLastError());
+}
+
 // Host-buffer entry: cached device buffers per shape, pinned staging.
 namespace {
 std::mutex g_host_mu;

@@ -19,6 +19,8 @@ struct DevState {
   std::atomic<bool> est_attr{false};   // k_estimate_batch
   std::atomic<bool> ssim_init{false};  // c_gauss taps + k_ssim_tiles attribute
   std::atomic<bool> mask_attr{false};  // k_mask_blocks attribute
+  std::atomic<bool> stage_attr{false};  // k_stages (estimator stages API)
+  std::atomic<bool> select_attr{false};  // k_select (select_and_estimate API)
 };
 
 inline int current_device() {

@@ -83,6 +83,7 @@ struct CellSmem {
   long long t_start, t_mark, t_pick, t_gather, t_g[4];
   int idl_diag;
   unsigned long long cnt[8];  // BRL IDL HQL deferred | flop64 flop32 hql gate
+  bm_patch_record rec;        // the current patch's LayerDecision (profiles.py:174-188)
   EstSmem est;
   HqlSmem hql;
   HqlOut hout;
@@ -360,7 +361,7 @@ __device__ void load_tile(const KParams& P, CellSmem& S) {
       const int ntr = tr / BS, ntc = tc / BS;
       const int nr = gr - 1 + ntr, nc = gc - 1 + ntc;
       int pslot = -1;
-      if ((ntr == 0 || (ntr == 1 && ntc == 0)) && nr >= 0 && nc >= 0 && nc < P.GC)
+      if (P.slotmap && (ntr == 0 || (ntr == 1 && ntc == 0)) && nr >= 0 && nc >= 0 && nc < P.GC)
         pslot = P.slotmap[((size_t)f * P.GR + nr) * P.GC + nc];
       if (pslot >= 0) {  // finished earlier-raster neighbour: its final values
         v = __ldcg(&P.cellbuf[(size_t)pslot * 256 + (tr % BS) * BS + (tc % BS)]);
@@ -503,7 +504,8 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   g.B1 = c1 - 4;
   if (warp == 0) {
     int mr, K;
-    if (r0 == br - BS && c0 == bc - BS && r1 == br + 2 * BS && c1 == bc + 2 * BS) {
+    if (P.ringtab && ((pr_t | pc_t) & 1) == 0 && r0 == br - BS && c0 == bc - BS && r1 == br + 2 * BS &&
+        c1 == bc + 2 * BS) {
       // interior cell: the patch position's ring offsets from the table
       // (k_sched_prep; the geometry is translation invariant)
       const int* t = P.ringtab + (size_t)((pr_t - BS) / 2 * 8 + (pc_t - BS) / 2) * 33;
@@ -511,7 +513,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
       mr = t[32];
       K = t[31];
     } else {
-      const int cnt = (lane >= 1 && lane <= 26) ? ring_count(g, lane) : 0;
+      const int cnt = (lane >= 1 && lane <= 28) ? ring_count(g, lane) : 0;
       int inc = cnt;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -638,14 +640,15 @@ __device__ void write_record(const KParams& P, CellSmem& S, const bm_patch_recor
   if (P.records) P.records[(size_t)S.slot * 64 + S.nrec] = rec;
 }
 
-// One patch: gate + estimate (select_and_estimate / _forced_estimate).
-__device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS) {
+// One patch at tile position (pr_t, pc_t): gate + estimate
+// (select_and_estimate / _forced_estimate, profiles.py:105-171) into E.vals
+// and S.rec; no write-back.
+__device__ void estimate_only(const KParams& P, CellSmem& S, int pr_t, int pc_t, double* gS) {
   const int tid = threadIdx.x;
   EstSmem& E = S.est;
-  const int pr_t = patch_r(p), pc_t = patch_c(p);
   const int forced = P.forced;
   const bool brl = forced >= 0 ? forced == BM_LAYER_BRL : S.phi <= P.t_phi;
-  __shared__ bm_patch_record rec;
+  bm_patch_record& rec = S.rec;
   if (tid == 0) {
     memset(&rec, 0, sizeof(rec));
     rec.frame = S.f;
@@ -781,7 +784,14 @@ __device__ void estimate_patch(const KParams& P, CellSmem& S, int p, double* gS)
     }
     __syncthreads();
   }
-  // write back (profiles.py:229-235) + record
+}
+
+// _write_patch (profiles.py:229-235) of patch p of the cell + its record.
+__device__ void commit_patch(const KParams& P, CellSmem& S, int p) {
+  const int tid = threadIdx.x;
+  EstSmem& E = S.est;
+  const int pr_t = patch_r(p), pc_t = patch_c(p);
+  bm_patch_record& rec = S.rec;
   if (tid < 4) {
     const int o = (pr_t + (tid >> 1)) * TS + pc_t + (tid & 1);
     const bool lost = S.st[o] == ST_LO;
@@ -906,6 +916,81 @@ __device__ void pick_and_extract(CellSmem& S) {
   }
 }
 
+// A TargetContext supplied by the caller (the per-patch library API,
+// framework.py:60-77): usable bits over CONTEXT_OFFSETS and y0 in layout
+// order, instead of pick_and_extract's extraction.  Warp 0.
+__device__ void set_target(CellSmem& S, unsigned layout, const double* __restrict__ y0g) {
+  const int lane = threadIdx.x & 31;
+  EstSmem& E = S.est;
+  const bool usable = (layout >> lane) & 1u;
+  const int n = __popc(layout);
+  double yv = 0.0;
+  if (usable) {
+    const int idx = __popc(layout & ((1u << lane) - 1));
+    yv = y0g[idx];
+    E.y0[idx] = yv;
+    E.y0f[idx] = (float)yv;
+    E.uoff[idx] = (int16_t)(ctx_r(lane) * TS + ctx_c(lane));
+  }
+  if (lane < 6) {  // window row masks (see pick_and_extract)
+    const int sh = lane < 2 ? 6 * lane : (lane < 4 ? 12 + 4 * (lane - 2) : 20 + 6 * (lane - 4));
+    const unsigned b = layout >> sh;
+    S.rowmask[lane] = (lane == 2 || lane == 3) ? ((b & 3u) | ((b & 0xCu) << 2) | 0xCu) : (b & 0x3Fu);
+  }
+  if (lane < 4) E.uoff[n + lane] = (int16_t)((2 + (lane >> 1)) * TS + 2 + (lane & 1));
+  const double ymax = warp_max(usable ? yv : -INFINITY), ymin = warp_min(usable ? yv : INFINITY);
+  __syncwarp();
+  if (lane == 0) {
+    E.n = n;
+    S.skip = n == 0;
+    S.phi = ymax - ymin;  // flatness (profiles.py:98-102)
+  }
+}
+
+// select_and_estimate (profiles.py:105-133), or _forced_estimate
+// (profiles.py:141-171) with P.forced >= 0, for independent patches of one
+// working image (P.pixels f64 [H,W], P.states): one CTA per patch, the same
+// device code as the fused kernel's patch step, no write-back.  The caller's
+// TargetContext (layout bits, y0) defines the context.
+struct SelectArgs {
+  int count;
+  const int32_t* origins;   // [count][2] patch origins (absolute)
+  const uint32_t* layouts;  // [count]
+  const double* y0;         // [count][32]
+  double* out_values;       // [count][4]
+  bm_patch_record* out_rec; // [count]
+};
+
+__global__ void __launch_bounds__(NT, 1) k_select(KParams P, SelectArgs A) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CellSmem& S = *reinterpret_cast<CellSmem*>(smem_raw);
+  const int tid = threadIdx.x, i = blockIdx.x;
+  if (i >= A.count) return;
+  if (tid < 8) S.cnt[tid] = 0;
+  init_exptab(S.est);
+  const int pr = A.origins[2 * i], pc = A.origins[2 * i + 1];
+  if (tid == 0) {
+    S.f = 0;
+    S.gr = pr / BS;  // block_origin_of (framework.py:114-116)
+    S.gc = pc / BS;
+    S.slot = 0;
+    S.nrec = 0;
+    S.idl_diag = 0;
+    S.t_start = clock64();
+  }
+  __syncthreads();
+  load_tile(P, S);
+  const int pr_t = pr - (S.gr * BS - BS), pc_t = pc - (S.gc * BS - BS);
+  if (tid < 32) set_target(S, A.layouts[i], A.y0 + (size_t)i * 32);
+  __syncthreads();
+  estimate_only(P, S, pr_t, pc_t, nullptr);
+  if (tid == 0) {
+    S.rec.cycles = (uint32_t)(clock64() - S.t_start);
+    A.out_rec[i] = S.rec;
+    for (int q = 0; q < 4; q++) A.out_values[(size_t)i * 4 + q] = S.est.vals[q];
+  }
+}
+
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CellSmem& S = *reinterpret_cast<CellSmem*>(smem_raw);
@@ -979,7 +1064,8 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
           __syncthreads();
           continue;
         }
-        estimate_patch(P, S, S.pick, gS);
+        estimate_only(P, S, patch_r(S.pick), patch_c(S.pick), gS);
+        commit_patch(P, S, S.pick);
         if (tid == 0) S.progressed = 1;
         __syncthreads();
       }

@@ -284,6 +284,76 @@ def decisions_from_records(recs: np.ndarray, clock_khz: int) -> list[LayerDecisi
     return out
 
 
+def select_and_estimate_batch(img, mask, targets, profile: Profile, sigma2: float = DEFAULT_SIGMA2, *,
+                              forced_layer: Layer | None = None) -> list:
+    """select_and_estimate (or _forced_estimate with forced_layer) for many
+    patches of one working image in one device call (bm_select_and_estimate:
+    the fused kernel's patch step, one CTA per patch, no write-back)."""
+    from .errors import EmptyContextError
+    from .estimators import BandwidthParams, EstimateDiagnostics, PatchEstimate
+
+    if not targets:
+        return []
+    for t in targets:
+        if t.n_y < 1:
+            raise EmptyContextError("flatness needs at least one context sample")
+    torch = _native.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    pixels = np.asarray(img.pixels if isinstance(img, ImageBuffer) else img, dtype=np.float64)
+    states = np.asarray(mask.states if isinstance(mask, LossMask) else mask, dtype=np.uint8)
+    require_same_shape(pixels, states)
+    n = len(targets)
+    origins = np.array([t.patch_origin for t in targets], dtype=np.int32).reshape(n, 2)
+    layouts = np.array([t.layout_bits() for t in targets], dtype=np.uint32)
+    y0 = np.zeros((n, 32))
+    for i, t in enumerate(targets):
+        y0[i, : t.n_y] = t.y0
+    h, w = pixels.shape
+    params = make_params(1, h, w, 1, profile, sigma2, forced_layer)
+
+    def put(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+    t_px, t_st, t_o, t_l, t_y = put(pixels), put(states), put(origins), put(layouts.view(np.int32)), put(y0)
+    vals = torch.empty((n, 4), dtype=torch.float64, device=dev)
+    rec = torch.empty((n, RECORD_DTYPE.itemsize), dtype=torch.uint8, device=dev)
+    _native.check(_native.lib().bm_select_and_estimate(
+        params, t_px.data_ptr(), t_st.data_ptr(), n, t_o.data_ptr(), t_l.data_ptr(), t_y.data_ptr(),
+        vals.data_ptr(), rec.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    vals = vals.cpu().numpy()
+    recs = rec.cpu().numpy().view(RECORD_DTYPE).reshape(-1)
+    hz = max(1, int(_native.lib().bm_device_clock_khz())) * 1e3
+    out = []
+    for i in range(n):
+        r = recs[i]
+        f = decode_flags(r)
+        layer = CODE_LAYER[int(r["layer"])]
+        bw = None
+        if f["has_bw"]:
+            bw = BandwidthParams(float(r["beta"]), float(r["alpha"]), None)
+        elif layer is Layer.IDL:
+            bw = BandwidthParams(None, None, sigma2)
+        diag = EstimateDiagnostics(
+            phi=float(r["phi"]) if f["has_phi"] else None,
+            nu=float(r["nu"]) if f["has_nu"] else None,
+            m_candidates=int(r["m_candidates"]) if f["has_m"] else None,
+            rings_used=int(r["rings_used"]),
+            bandwidth=bw,
+            elapsed_s=float(r["cycles"]) / hz,
+            fallback=f["fallback"],
+            beta_gap=float(r["beta_gap"]) if f["has_bw"] else None,
+        )
+        out.append(PatchEstimate(vals[i].copy(), layer, diag))
+    return out
+
+
+def select_and_estimate(img, mask, target, profile: Profile, sigma2: float = DEFAULT_SIGMA2):
+    """Pick and run the cheapest suitable layer for one patch (profiles.py:105-133):
+    phi <= T_phi -> BRL; else the ring-by-ring support expansion with the
+    cumulative nu; nu >= T_nu -> IDL, else HQL with its ladder."""
+    return select_and_estimate_batch(img, mask, [target], profile, sigma2)[0]
+
+
 def conceal_image(
     img: ImageBuffer,
     mask: LossMask,
@@ -341,4 +411,6 @@ __all__ = [
     "conceal_image",
     "decisions_from_records",
     "make_params",
+    "select_and_estimate",
+    "select_and_estimate_batch",
 ]
