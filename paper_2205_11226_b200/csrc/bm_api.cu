@@ -245,25 +245,36 @@ __global__ void k_emap(int H, int W, int count, const int32_t* __restrict__ orig
 // NumPy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src
 // pairwise_sum) of a contiguous double array: < 8 sequential, <= 128 eight
 // accumulators, else split at n/2 rounded down to a multiple of 8.
-__device__ double np_pairwise_sum(const double* a, int n, int stride = 1) {
+__device__ __noinline__ double np_pairwise_leaf(const double* a, int n, int stride) {
   if (n < 8) {
     double res = 0.0;
     for (int i = 0; i < n; i++) res += a[(size_t)i * stride];
     return res;
   }
-  if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; j++) r[j] = a[(size_t)j * stride];
-    int i = 8;
-    for (; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; j++) r[j] += a[(size_t)(i + j) * stride];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; i++) res += a[(size_t)i * stride];
-    return res;
-  }
+  double r[8];
+  for (int j = 0; j < 8; j++) r[j] = a[(size_t)j * stride];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; j++) r[j] += a[(size_t)(i + j) * stride];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; i++) res += a[(size_t)i * stride];
+  return res;
+}
+// the recursion unrolled at compile time (D levels cover n <= 128 * 2^D;
+// no runtime recursion, so the stack size stays static)
+template <int D>
+__device__ __forceinline__ double np_pairwise(const double* a, int n, int stride) {
+  if (n <= 128) return np_pairwise_leaf(a, n, stride);
   int n2 = n / 2;
   n2 -= n2 % 8;
-  return np_pairwise_sum(a, n2, stride) + np_pairwise_sum(a + (size_t)n2 * stride, n - n2, stride);
+  return np_pairwise<D - 1>(a, n2, stride) + np_pairwise<D - 1>(a + (size_t)n2 * stride, n - n2, stride);
+}
+template <>
+__device__ __forceinline__ double np_pairwise<0>(const double* a, int n, int stride) {
+  return np_pairwise_leaf(a, n, stride);
+}
+__device__ __forceinline__ double np_pairwise_sum(const double* a, int n, int stride = 1) {
+  return np_pairwise<5>(a, n, stride);  // n <= 4096
 }
 
 struct StageSmem {

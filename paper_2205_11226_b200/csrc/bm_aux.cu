@@ -83,9 +83,10 @@ __global__ void k_reduce_frames(const double* part, const double* cnt, int nchun
   if (out_cnt) out_cnt[f] = n;
 }
 
-__global__ void k_scale(double* v, int n, double s) {
+// v[i] / d: the mean as NumPy forms it (sum / count, not sum * (1 / count))
+__global__ void k_div(double* v, int n, double d) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] *= s;
+  if (i < n) v[i] /= d;
 }
 
 // ---------------------------------------------------------------- SSIM
@@ -288,7 +289,7 @@ int bm_ssim_batch(const void* ref, const void* test, int pixel_dtype, int frames
                                                                    part);
   // per-frame totals in tile order (fixed), then the mean over the valid map
   k_reduce_frames<<<(frames + 127) / 128, 128, 0, st>>>(part, nullptr, ntile, frames, out_mean, nullptr);
-  k_scale<<<(frames + 127) / 128, 128, 0, st>>>(out_mean, frames, 1.0 / ((double)vh * (double)vw));
+  k_div<<<(frames + 127) / 128, 128, 0, st>>>(out_mean, frames, (double)vh * (double)vw);
   e = cudaGetLastError();
   cudaFreeAsync(part, st);
   return status(e);
