@@ -24,6 +24,10 @@ typedef struct {
 int orc_conceal(int H, int W, const double* pixels, const uint8_t* states, double t_phi, double t_nu,
                 double sigma2, int forced_layer, double* out_pixels, orc_record* out_records,
                 long max_records, long* out_nrec, long* out_lost_cells);
+/* the same with the cells of each dependency level on `threads` threads */
+int orc_conceal_dag(int H, int W, const double* pixels, const uint8_t* states, double t_phi, double t_nu,
+                    double sigma2, int forced_layer, double* out_pixels, orc_record* out_records,
+                    long max_records, long* out_nrec, long* out_lost_cells, int threads);
 void orc_brl(const double* y0, int n, double* out4);
 int orc_idl(const double* y0, int n, const double* x, const double* y, int m, double sigma2,
             double* out4, double* raw_sum);

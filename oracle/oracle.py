@@ -78,6 +78,8 @@ def lib():
             ctypes.c_double, ctypes.c_int, dp, ctypes.c_void_p, ctypes.c_long,
             ctypes.POINTER(ctypes.c_long), ctypes.POINTER(ctypes.c_long),
         ]
+        _lib.orc_conceal_dag.restype = ctypes.c_int
+        _lib.orc_conceal_dag.argtypes = _lib.orc_conceal.argtypes + [ctypes.c_int]
         _lib.orc_hql.argtypes = [dp, ctypes.c_int, dp, dp, ctypes.c_int, ctypes.c_double, dp,
                                  ctypes.POINTER(_Info)]
         _lib.orc_idl.argtypes = [dp, ctypes.c_int, dp, dp, ctypes.c_int, ctypes.c_double, dp, dp]
@@ -102,6 +104,27 @@ def conceal(pixels, states, t_phi, t_nu, sigma2=10.0, forced_layer=-1):
     status = lib().orc_conceal(
         h, w, _dp(px), st.ctypes.data, float(t_phi), float(t_nu), float(sigma2), int(forced_layer),
         _dp(out), recs.ctypes.data, cap, ctypes.byref(nrec), ctypes.byref(cells),
+    )
+    return out, recs[: nrec.value].copy(), status, cells.value
+
+
+def conceal_dag(pixels, states, t_phi, t_nu, sigma2=10.0, forced_layer=-1, threads=None):
+    """conceal() with the cells of each dependency level concurrent on
+    `threads` threads (same result as the serial raster order); for
+    full-size parity frames."""
+    px = np.ascontiguousarray(pixels, dtype=np.float64)
+    st = np.ascontiguousarray(states, dtype=np.uint8)
+    h, w = px.shape
+    out = np.empty_like(px)
+    cap = (h // 16) * (w // 16) * 64 + 1
+    recs = np.zeros(cap, dtype=RECORD_DTYPE)
+    nrec = ctypes.c_long(0)
+    cells = ctypes.c_long(0)
+    if threads is None:
+        threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    status = lib().orc_conceal_dag(
+        h, w, _dp(px), st.ctypes.data, float(t_phi), float(t_nu), float(sigma2), int(forced_layer),
+        _dp(out), recs.ctypes.data, cap, ctypes.byref(nrec), ctypes.byref(cells), int(threads),
     )
     return out, recs[: nrec.value].copy(), status, cells.value
 

@@ -4,16 +4,25 @@ Implements the north_star bars (BASELINE.json) with SURVEY.md §8(d)'s
 divergence rule:
   * per-patch records are compared cell by cell in processing order:
     origin, layer, rings_used, m_candidates, N_y, deferral must match;
-  * a mismatch is ALLOWED only when it is decided at a threshold or by
-    rounding: |phi - T_phi| <= TOL*max(1,|T_phi|), |nu - T_nu| <= TOL*max(1,T_nu)
-    on either side's score, or a beta grid choice whose reference epsilon gap
-    (bm_patch_record.beta_gap: min |eps_g - eps_best| in units of the eps
-    change a 1e-11 relative input perturbation can cause) is below BETA_TIE,
-    i.e. the reference's beta choice is decided at rounding level;
-  * after an allowed divergence the rest of that cell and all of its
-    later-raster 8-neighbour descendants are excluded from pixel checks;
-  * on the remaining lost pixels: |d| <= 1e-3 * max(|ref|, 1) and the u8
-    outputs differ by at most 1 on at most 0.1% of concealed pixels.
+  * a LAYER-DECISION mismatch (layer, rings, M', N_y, deferral) is excused
+    only when the REFERENCE's complexity score is within TOL = 1e-5
+    (absolute) of its profile threshold: |phi - T_phi| <= 1e-5 or
+    |nu - T_nu| <= 1e-5 (the north_star's rule; the tested side's score is
+    not consulted);
+  * beta is an HQL parameter, not a layer decision.  A beta choice that
+    differs while the layer decision matches is counted as a beta tie when
+    the reference's own choice was decided at rounding level (its
+    beta_gap: min |eps_g - eps_best| in units of the eps change a 1e-11
+    relative input perturbation causes, < BETA_TIE); any other beta
+    difference is a failure;
+  * after an excused divergence (threshold or beta tie) the rest of that cell
+    and all its later-raster 8-neighbour descendants leave the per-pixel bar,
+    which holds on the remaining lost pixels: |d| <= 1e-3 * max(|ref|, 1),
+    u8 off by at most 1 on at most 0.1% of all lost pixels;
+  * the all-pixel figures (max |du8|, max rel, pixels off over EVERY lost
+    pixel, excluded cells included) are always reported, so the size of a
+    legitimate divergence is visible, and callers bound the number of
+    excused cells per case.
 """
 
 from __future__ import annotations
@@ -32,20 +41,24 @@ REL = 1e-3
 class ParityResult:
     ok: bool
     problems: list = field(default_factory=list)
-    allowed: list = field(default_factory=list)
+    allowed: list = field(default_factory=list)  # threshold-decided layer divergences
+    beta_ties: list = field(default_factory=list)  # rounding-decided beta choices of the reference
     excluded_cells: set = field(default_factory=set)
     checked_pixels: int = 0
     u8_off: int = 0
     max_rel: float = 0.0
     max_u8: int = 0
-    u8_off_all: int = 0  # over ALL lost pixels, excluded cells included
     lost_pixels: int = 0
+    u8_off_all: int = 0  # over ALL lost pixels, excluded cells included
+    max_u8_all: int = 0
+    max_rel_all: float = 0.0
 
     def summary(self) -> str:
-        return (f"ok={self.ok} problems={len(self.problems)} allowed={len(self.allowed)} "
-                f"excluded_cells={len(self.excluded_cells)} checked_px={self.checked_pixels} "
-                f"u8_off={self.u8_off} max_u8={self.max_u8} max_rel={self.max_rel:.2e} "
-                f"u8_off_all={self.u8_off_all}/{self.lost_pixels}")
+        return (f"ok={self.ok} problems={len(self.problems)} threshold={len(self.allowed)} "
+                f"beta_ties={len(self.beta_ties)} excluded_cells={len(self.excluded_cells)} "
+                f"checked_px={self.checked_pixels} u8_off={self.u8_off} max_u8={self.max_u8} "
+                f"max_rel={self.max_rel:.2e} | all lost px: u8_off={self.u8_off_all}/{self.lost_pixels} "
+                f"max_u8={self.max_u8_all} max_rel={self.max_rel_all:.2e}")
 
 
 def _cells_of(recs):
@@ -56,10 +69,16 @@ def _cells_of(recs):
     return out
 
 
-def _near(score, thr):
+def _near(score, thr) -> bool:
     if score is None or not np.isfinite(score) or not np.isfinite(thr):
         return False
-    return abs(score - thr) <= TOL * max(1.0, abs(thr))
+    return abs(score - thr) <= TOL
+
+
+def _rel_u8(a, b):
+    rel = np.abs(a - b) / np.maximum(np.abs(a), 1.0)
+    dq = np.abs(np.floor(np.clip(a, 0, 255) + 0.5) - np.floor(np.clip(b, 0, 255) + 0.5))
+    return rel, dq
 
 
 def compare(ref_out, ref_recs, test_out, test_recs, states, t_phi, t_nu) -> ParityResult:
@@ -96,57 +115,54 @@ def compare(ref_out, ref_recs, test_out, test_recs, states, t_phi, t_nu) -> Pari
                 res.ok = False
                 res.problems.append(f"{where}: origin {int(b['row'])},{int(b['col'])}")
                 break
-            same = (a["layer"] == b["layer"] and a["rings_used"] == b["rings_used"]
-                    and a["m_candidates"] == b["m_candidates"] and a["n_y"] == b["n_y"]
-                    and (int(a["flags"]) & 3) == (int(b["flags"]) & 3))
+            decision_same = (a["layer"] == b["layer"] and a["rings_used"] == b["rings_used"]
+                             and a["m_candidates"] == b["m_candidates"] and a["n_y"] == b["n_y"]
+                             and (int(a["flags"]) & 3) == (int(b["flags"]) & 3))
             beta_same = (a["beta"] == b["beta"]) or (math.isnan(a["beta"]) and math.isnan(b["beta"]))
-            if same and beta_same:
+            if decision_same and beta_same:
                 continue
-            excuse = None
-            if a["n_y"] == b["n_y"] and (_near(a["phi"], t_phi) or _near(b["phi"], t_phi)):
-                excuse = "phi at T_phi"
-            elif a["n_y"] == b["n_y"] and (_near(a["nu"], t_nu) or _near(b["nu"], t_nu)):
-                excuse = "nu at T_nu"
-            elif same and not beta_same and float(a["beta_gap"]) < BETA_TIE:
-                excuse = f"beta near-tie (gap {float(a['beta_gap']):.1e})"
-            if excuse is None:
-                res.ok = False
-                res.problems.append(
-                    f"{where}: ref layer={int(a['layer'])} rings={int(a['rings_used'])} m={int(a['m_candidates'])} "
-                    f"ny={int(a['n_y'])} beta={a['beta']} phi={a['phi']} nu={a['nu']} | test layer={int(b['layer'])} "
-                    f"rings={int(b['rings_used'])} m={int(b['m_candidates'])} ny={int(b['n_y'])} beta={b['beta']} "
-                    f"phi={b['phi']} nu={b['nu']}")
+            detail = (f"ref layer={int(a['layer'])} rings={int(a['rings_used'])} m={int(a['m_candidates'])} "
+                      f"ny={int(a['n_y'])} beta={a['beta']} phi={a['phi']} nu={a['nu']} | test "
+                      f"layer={int(b['layer'])} rings={int(b['rings_used'])} m={int(b['m_candidates'])} "
+                      f"ny={int(b['n_y'])} beta={b['beta']} phi={b['phi']} nu={b['nu']}")
+            if not decision_same:
+                if a["n_y"] == b["n_y"] and (_near(a["phi"], t_phi) or _near(a["nu"], t_nu)):
+                    res.allowed.append(f"{where}: reference score at its threshold: {detail}")
+                else:
+                    res.ok = False
+                    res.problems.append(f"{where}: {detail}")
+            elif float(a["beta_gap"]) < BETA_TIE:
+                res.beta_ties.append(f"{where}: reference beta decided at rounding level "
+                                     f"(gap {float(a['beta_gap']):.2e}): {detail}")
             else:
-                res.allowed.append(f"{where}: {excuse}")
+                res.ok = False
+                res.problems.append(f"{where}: beta differs (gap {float(a['beta_gap']):.2e}): {detail}")
             excl.add(cell)
             break
     res.excluded_cells = excl
     lost = states == 1
     res.lost_pixels = int(lost.sum())
-    qa_all = np.floor(np.clip(ref_out[lost], 0, 255) + 0.5)
-    qb_all = np.floor(np.clip(test_out[lost], 0, 255) + 0.5)
-    res.u8_off_all = int((qa_all != qb_all).sum())
+    if res.lost_pixels:
+        rel_all, dq_all = _rel_u8(ref_out[lost], test_out[lost])
+        res.u8_off_all = int((dq_all > 0).sum())
+        res.max_u8_all = int(dq_all.max())
+        res.max_rel_all = float(rel_all.max())
     keep = lost.copy()
     for f, r, c in excl:
         keep[f, r * 16 : (r + 1) * 16, c * 16 : (c + 1) * 16] = False
     n = int(keep.sum())
     res.checked_pixels = n
     if n:
-        a = ref_out[keep]
-        b = test_out[keep]
-        rel = np.abs(a - b) / np.maximum(np.abs(a), 1.0)
+        rel, dq = _rel_u8(ref_out[keep], test_out[keep])
         res.max_rel = float(rel.max())
-        qa = np.floor(np.clip(a, 0, 255) + 0.5)
-        qb = np.floor(np.clip(b, 0, 255) + 0.5)
-        dq = np.abs(qa - qb)
         res.u8_off = int((dq > 0).sum())
         res.max_u8 = int(dq.max())
         if res.max_rel > REL:
             res.ok = False
             res.problems.append(f"float rel diff {res.max_rel:.3e} > {REL}")
-        if res.max_u8 > 1 or res.u8_off > 0.001 * int(lost.sum()):
+        if res.max_u8 > 1 or res.u8_off > 0.001 * res.lost_pixels:
             res.ok = False
-            res.problems.append(f"u8: {res.u8_off} px off (max {res.max_u8}) of {int(lost.sum())} lost")
+            res.problems.append(f"u8: {res.u8_off} px off (max {res.max_u8}) of {res.lost_pixels} lost")
     # non-lost pixels must be untouched
     if not np.array_equal(ref_out[~lost], test_out[~lost]):
         res.ok = False

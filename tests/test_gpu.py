@@ -96,6 +96,10 @@ CFG_CASES = [
 ]
 
 
+# measured excused divergences (threshold decisions + reference beta ties) per case
+EXCUSED_MAX = {"cfg1_full": 4, "cfg2_full": 1}
+
+
 @pytest.mark.parametrize("build", BUILDS)
 @pytest.mark.parametrize("case", CFG_CASES, ids=[c[0] for c in CFG_CASES])
 def test_config_parity_vs_oracle(native, case, build):
@@ -131,10 +135,11 @@ def test_config_parity_vs_oracle(native, case, build):
     pr = parity.compare(o_out, o_rec, gout, grec, st, prof.t_phi, prof.t_nu)
     assert pr.ok, pr.problems[:5]
     print(case[0], build, pr.summary())
-    # excluded (legitimately diverged) cells must stay rare, and even counting
-    # them the u8 outputs stay within the +-1 LSB on <= 0.1% bar... up to the
-    # rounding-decided beta flips of the all-HQL sentinel profile
-    assert len(pr.excluded_cells) <= max(2, 0.10 * res.summary["lost_cells"]), pr.allowed
+    # excused divergences per case, bounded by the measured counts (DESIGN.md
+    # §5): layer decisions at a threshold and the reference's rounding-decided
+    # beta choices; everything else must match exactly
+    excused = len(pr.allowed) + len(pr.beta_ties)
+    assert excused <= EXCUSED_MAX.get(case[0], 0), (pr.allowed, pr.beta_ties)
     assert res.summary["patches"] == len(o_rec)
 
 
