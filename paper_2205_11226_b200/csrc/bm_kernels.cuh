@@ -786,48 +786,53 @@ __device__ void estimate_only(const KParams& P, CellSmem& S, int pr_t, int pc_t,
   }
 }
 
-// _write_patch (profiles.py:229-235) of patch p of the cell + its record.
+// _write_patch (profiles.py:229-235) of patch p of the cell + its record, on
+// warp 0 (write-back, the 8 neighbours' schedule keys, the LOST bitmap rows,
+// the record), then one CTA barrier.
 __device__ void commit_patch(const KParams& P, CellSmem& S, int p) {
   const int tid = threadIdx.x;
-  EstSmem& E = S.est;
-  const int pr_t = patch_r(p), pc_t = patch_c(p);
-  bm_patch_record& rec = S.rec;
-  if (tid < 4) {
-    const int o = (pr_t + (tid >> 1)) * TS + pc_t + (tid & 1);
-    const bool lost = S.st[o] == ST_LO;
-    if (lost) {
-      S.tile[o] = E.vals[tid];
-      S.tile32[o] = (float)E.vals[tid];
-      S.st[o] = ST_RE;
+  if (tid < 32) {
+    EstSmem& E = S.est;
+    const int pr_t = patch_r(p), pc_t = patch_c(p);
+    bm_patch_record& rec = S.rec;
+    bool lost = false;
+    if (tid < 4) {
+      const int o = (pr_t + (tid >> 1)) * TS + pc_t + (tid & 1);
+      lost = S.st[o] == ST_LO;
+      if (lost) {
+        S.tile[o] = E.vals[tid];
+        S.tile32[o] = (float)E.vals[tid];
+        S.st[o] = ST_RE;
+      }
     }
-    const unsigned wl = __ballot_sync(0xFu, lost);
-    if (tid == 0) S.wb_lost = __popc(wl);
-  }
-  __syncthreads();
-  if (tid >= 32 && tid < 40) {  // the 8 neighbouring patches gain usable context
-    const int k = tid - 32, d = k < 4 ? k : k + 1;  // 3x3 neighbourhood minus the centre
-    const int qr = (p >> 3) + d / 3 - 1, qc = (p & 7) + d % 3 - 1;
-    if (qr >= 0 && qr < 8 && qc >= 0 && qc < 8) S.pkey[qr * 8 + qc] += S.wb_lost << 7;
-  }
-  if (tid < 2) {
-    const int r = pr_t + tid;
-    uint64_t b = S.lostbits[r];
-    b &= ~(3ull << pc_t);
-    b |= (uint64_t)(S.st[r * TS + pc_t] == ST_LO) << pc_t;
-    b |= (uint64_t)(S.st[r * TS + pc_t + 1] == ST_LO) << (pc_t + 1);
-    S.lostbits[r] = b;
-  }
-  if (tid == 0) {
-    if (S.idl_diag) {
-      BM_DIAG_ADD(19, (clock64() - S.t_mark));
-      S.idl_diag = 0;
+    const int wb_lost = __popc(__ballot_sync(FULL, lost));
+    __syncwarp();
+    if (tid >= 8 && tid < 16) {  // the 8 neighbouring patches gain usable context
+      const int k = tid - 8, d = k < 4 ? k : k + 1;  // 3x3 neighbourhood minus the centre
+      const int qr = (p >> 3) + d / 3 - 1, qc = (p & 7) + d % 3 - 1;
+      if (qr >= 0 && qr < 8 && qc >= 0 && qc < 8) S.pkey[qr * 8 + qc] += wb_lost << 7;
     }
-    rec.cycles = (uint32_t)(clock64() - S.t_start);
-    if (rec.layer >= BM_LAYER_IDL) BM_DIAG_ADD(13 + rec.layer, rec.cycles);
-    else BM_DIAG_ADD(21, rec.cycles);
-    write_record(P, S, rec);
-    S.nrec++;
-    S.cnt[rec.layer]++;
+    if (tid < 2) {
+      const int r = pr_t + tid;
+      uint64_t b = S.lostbits[r];
+      b &= ~(3ull << pc_t);
+      b |= (uint64_t)(S.st[r * TS + pc_t] == ST_LO) << pc_t;
+      b |= (uint64_t)(S.st[r * TS + pc_t + 1] == ST_LO) << (pc_t + 1);
+      S.lostbits[r] = b;
+    }
+    if (tid == 0) {
+      if (S.idl_diag) {
+        BM_DIAG_ADD(19, (clock64() - S.t_mark));
+        S.idl_diag = 0;
+      }
+      rec.cycles = (uint32_t)(clock64() - S.t_start);
+      if (rec.layer >= BM_LAYER_IDL) BM_DIAG_ADD(13 + rec.layer, rec.cycles);
+      else BM_DIAG_ADD(21, rec.cycles);
+      write_record(P, S, rec);
+      S.nrec++;
+      S.cnt[rec.layer]++;
+      S.progressed = 1;
+    }
   }
   __syncthreads();
 }
@@ -1065,9 +1070,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
           continue;
         }
         estimate_only(P, S, patch_r(S.pick), patch_c(S.pick), gS);
-        commit_patch(P, S, S.pick);
-        if (tid == 0) S.progressed = 1;
-        __syncthreads();
+        commit_patch(P, S, S.pick);  // ends with a CTA barrier
       }
       if (S.ndef == 0) break;
       if (S.progressed) {
