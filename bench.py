@@ -341,7 +341,8 @@ def measure(args, ctx, frame_range, n_total):
         if args.stub:
             gather.local.copy_(px)
         else:
-            conceal_batch(px, st, prof, forced_layer=forced, out_u8=gather.local, sync=False, time_kernel=True)
+            conceal_batch(px, st, prof, forced_layer=forced, out_u8=gather.local, sync=False, time_kernel=True,
+                          kernel_build=kbuild(args))
         gather.gather()  # the result gather to rank 0 (the path's only collective)
 
     for _ in range(args.warmup):
@@ -371,7 +372,8 @@ def measure(args, ctx, frame_range, n_total):
         summ = {"lost_cells": int(px.shape[0]), "patches": 0, "layer_counts": {}, "max_level": 0,
                 "flop64": 0, "flop32": 0}
     else:  # counts / algorithmic work of one (deterministic) step
-        summ = conceal_batch(px, st, prof, forced_layer=forced, out_u8=gather.local, sync=True).summary
+        summ = conceal_batch(px, st, prof, forced_layer=forced, out_u8=gather.local, sync=True,
+                             kernel_build=kbuild(args)).summary
     frames = gather.frames()
     if frames is not None and ctx["rank"] == 0:
         assert frames.shape[0] == n_total
@@ -380,6 +382,18 @@ def measure(args, ctx, frame_range, n_total):
             assert torch.equal(frames[:, 0, 0].to(torch.int64), want), "result gather out of order"
     return {"px_np": px_np, "st_np": st_np, "step_ms": step_ms, "kms": kms, "summ": summ,
             "clocks": clk.summary() if cuda else None, "px": px}
+
+
+def kbuild(args):
+    b = args.kernel_build
+    return None if b == "auto" else (int(b) if b.isdigit() else b)
+
+
+def build_flags(args) -> int:
+    from paper_2205_11226_b200 import _native
+
+    return {"auto": 0, "256": _native.BM_FLAG_BUILD_256, "512": _native.BM_FLAG_BUILD_512,
+            "cluster": _native.BM_FLAG_BUILD_CLUSTER, "narrow512": _native.BM_FLAG_NARROW_512}[args.kernel_build]
 
 
 class _Null:
@@ -413,6 +427,8 @@ def main():
                     help="auto (default): batch configs shard the config's own batch by frame range over the N "
                          "ranks (strong scaling) and also report weak scaling (every rank its own batch of the "
                          "config's size) in `secondary`; single-image configs run one replica per GPU")
+    ap.add_argument("--kernel-build", default="auto", choices=["auto", "256", "512", "cluster", "narrow512"],
+                    help="concealment kernel build (default: chosen on the device from the DAG shape)")
     ap.add_argument("--stub", action="store_true", help=argparse.SUPPRESS)  # CPU launcher test (gloo, no GPU)
     args = ap.parse_args()
 
@@ -485,6 +501,7 @@ def main():
 
         lib = _native.lib()
         params = make_params(px.shape[0], px.shape[1], px.shape[2], 0, prof, 10.0, forced)
+        params.flags |= build_flags(args)
         h_px = torch.from_numpy(px_np).pin_memory()
         h_st = torch.from_numpy(st_np).pin_memory()
         h_out = torch.empty_like(h_px).pin_memory()

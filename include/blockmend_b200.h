@@ -110,6 +110,11 @@ typedef struct bm_summary {
  * can differ in the last bits between builds (tests, A/B). */
 #define BM_FLAG_BUILD_256 2
 #define BM_FLAG_BUILD_512 4
+/* the cluster build: 2-CTA thread-block clusters of 512 threads per cell, the
+ * HQL candidate loops split across the two SMs over distributed shared memory */
+#define BM_FLAG_BUILD_CLUSTER 8
+/* narrow DAGs (default choice): the 512-thread build instead of the cluster build */
+#define BM_FLAG_NARROW_512 16
 
 /* ---- queries ---- */
 int bm_abi_version(void);

@@ -16,7 +16,8 @@ from .errors import DimensionMismatchError, NativeUnavailableError
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG_DIR, "_blockmend_b200.so")
-SOURCES = [os.path.join(PKG_DIR, "csrc", f) for f in ("bm_conceal.cu", "bm_conceal_wide.cu", "bm_aux.cu", "bm_api.cu")]
+SOURCES = [os.path.join(PKG_DIR, "csrc", f)
+           for f in ("bm_conceal.cu", "bm_conceal_wide.cu", "bm_conceal_cluster.cu", "bm_aux.cu", "bm_api.cu")]
 HEADERS = sorted(glob.glob(os.path.join(PKG_DIR, "csrc", "*.cuh")) + glob.glob(os.path.join(PKG_DIR, "csrc", "*.h"))) + [
     os.path.join(os.path.dirname(PKG_DIR), "include", "blockmend_b200.h")
 ]
@@ -27,7 +28,7 @@ NVCC_FLAGS = [
 ]
 
 BM_FLAG_TIME_KERNEL = 1
-BM_FLAG_BUILD_256, BM_FLAG_BUILD_512 = 2, 4
+BM_FLAG_BUILD_256, BM_FLAG_BUILD_512, BM_FLAG_BUILD_CLUSTER, BM_FLAG_NARROW_512 = 2, 4, 8, 16
 BM_OK, BM_ERR_ARGS, BM_ERR_LOST_LEFT, BM_ERR_CUDA, BM_ERR_WORKSPACE, BM_ERR_STATES = 0, 1, 2, 3, 4, 5
 
 

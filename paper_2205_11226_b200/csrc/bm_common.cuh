@@ -17,6 +17,17 @@ namespace BM_NS {
 #endif
 constexpr int NT = BM_NT;        // threads per concealment CTA (2 CTAs = 2 cells per SM, 128 regs)
 constexpr int NWARP = NT / 32;
+#ifndef BM_CS
+#define BM_CS 1
+#endif
+// CTAs per thread-block cluster that share one cell (bm_conceal_cluster.cu):
+// every CTA of the cluster runs the cell's control flow on identical data, the
+// candidate loops of the HQL pipeline are split over the cluster's warps
+// (global warp index rank * NWARP + warp) and the partial results are
+// combined over distributed shared memory in rank order, so every CTA holds
+// the same bits.  1 = no cluster.
+constexpr int CS = BM_CS;
+constexpr int GWARPS = CS * NWARP;  // warps sharing a cell's candidate loops
 constexpr int BS = 16;           // BLOCK_SIZE (image.py:18)
 constexpr int TILE = 48;         // 3x3-cell support area (framework.py:119-127)
 #ifndef BM_TS
@@ -199,6 +210,43 @@ __device__ __forceinline__ void ring_entry(const RingGeom& g, int r, int i, int&
   const int a_side = m0 + (i2 >> sh), b_side = (lv && (i2 & sh) == 0) ? g.pc - d : g.pc + d;
   a = first ? a_sq : (i2 < 0 ? g.pr - d : (i3 < 0 ? a_side : g.pr + d));
   b = first ? b_sq : (i2 < 0 ? b0 + i : (i3 < 0 ? b_side : b0 + i3));
+}
+
+// ---- thread-block cluster / distributed shared memory (CS > 1) ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ unsigned cluster_rank() {
+  if constexpr (CS == 1) {
+    return 0;
+  } else {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+  }
+}
+// every thread of every CTA of the cluster; release / acquire at cluster scope
+__device__ __forceinline__ void cluster_sync_all() {
+  if constexpr (CS > 1) {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
+}
+// shared::cluster address of `p` (a shared-memory object of this CTA) in CTA `rank`
+__device__ __forceinline__ uint32_t map_rank(const void* p, unsigned rank) {
+  uint32_t o;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(smem_u32(p)), "r"(rank));
+  return o;
+}
+__device__ __forceinline__ double ld_dsmem_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_dsmem_s32(uint32_t a) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_dsmem_f64(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {

@@ -39,14 +39,26 @@ size_t cell_smem_bytes();
 int threads();
 cudaError_t set_smem(size_t smem);
 cudaError_t launch(const void* P, int grid, size_t smem, cudaStream_t stream);
+cudaError_t add_phase_cycles(unsigned long long* out48, int reset);
 }  // namespace bm_wide
-static_assert(sizeof(bm::KParams) > 0, "KParams layout is shared by both builds");
+namespace bm_cluster {  // bm_conceal_cluster.cu: the 2-CTA cluster build of k_conceal
+size_t cell_smem_bytes();
+int cluster_size();
+cudaError_t set_smem(size_t smem);
+int max_clusters(size_t smem);
+cudaError_t launch(const void* P, int clusters, size_t smem, cudaStream_t stream);
+cudaError_t add_phase_cycles(unsigned long long* out48, int reset);
+}  // namespace bm_cluster
+static_assert(sizeof(bm::KParams) > 0, "KParams layout is shared by all builds");
 
 
 // =================================================================== C ABI
 using namespace bm;
 
 namespace {
+
+// the narrowest DAGs: the 2-CTA cluster build (1) or the 512-thread build (0) by default
+constexpr int NARROW_CLUSTER_DEFAULT = 1;
 
 struct Layout {
   size_t ncell;
@@ -143,11 +155,14 @@ extern "C" {
 int bm_abi_version(void) { return BM_ABI_VERSION; }
 
 int bm_debug_phase_cycles(unsigned long long* out48, int reset) {
+  // the three builds' counters added (only the build that ran has non-zero ones)
   if (cudaMemcpyFromSymbol(out48, g_phase_cycles, 48 * 8) != cudaSuccess) return BM_ERR_CUDA;
   if (reset) {
     unsigned long long z[48] = {0};
     cudaMemcpyToSymbol(g_phase_cycles, z, 48 * 8);
   }
+  if (bm_wide::add_phase_cycles(out48, reset) != cudaSuccess) return BM_ERR_CUDA;
+  if (bm_cluster::add_phase_cycles(out48, reset) != cudaSuccess) return BM_ERR_CUDA;
   return BM_OK;
 }
 
@@ -213,7 +228,9 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   P.t_nu = p->t_nu;
   P.sigma2 = p->sigma2;
   P.forced = p->forced_layer;
-  P.build = (p->flags & BM_FLAG_BUILD_512) ? 512 : ((p->flags & BM_FLAG_BUILD_256) ? 256 : 0);
+  P.build = (p->flags & BM_FLAG_BUILD_CLUSTER) ? BUILD_CLUSTER
+            : (p->flags & BM_FLAG_BUILD_512) ? 512 : ((p->flags & BM_FLAG_BUILD_256) ? 256 : 0);
+  P.narrow_cluster = (p->flags & BM_FLAG_NARROW_512) ? 0 : NARROW_CLUSTER_DEFAULT;
   P.pixels = pixels;
   P.states = states;
   P.out_f64 = out_f64;
@@ -270,6 +287,8 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
     }
     if (!D.attr_w.load()) {
       if ((e = bm_wide::set_smem(smem_w)) != cudaSuccess) return cuda_status(e);
+      if ((e = bm_cluster::set_smem(bm_cluster::cell_smem_bytes())) != cudaSuccess) return cuda_status(e);
+      D.clusters = bm_cluster::max_clusters(bm_cluster::cell_smem_bytes());
       D.attr_w = true;
     }
     const bool timed = (p->flags & BM_FLAG_TIME_KERNEL) != 0;
@@ -287,6 +306,8 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
     // both builds launch; each returns at once unless the DAG shape is its own
     k_conceal<<<L.grid, NT, smem, stream>>>(P);
     if ((e = bm_wide::launch(&P, sms, smem_w, stream)) != cudaSuccess) return cuda_status(e);
+    if ((e = bm_cluster::launch(&P, D.clusters, bm_cluster::cell_smem_bytes(), stream)) != cudaSuccess)
+      return cuda_status(e);
     if (timed) {
       cudaEventRecord(g_ev[slot_ev][1], stream);
       if (g_nev < NEV) g_nev++;

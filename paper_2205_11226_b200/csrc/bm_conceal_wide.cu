@@ -4,6 +4,7 @@
 // runs only on the DAG shapes it serves.
 #define BM_NT 512
 #define BM_NS bmw
+#define BM_CONCEAL_ONLY 1
 #include "bm_kernels.cuh"
 
 namespace bm_wide {
@@ -22,4 +23,19 @@ cudaError_t launch(const void* P, int grid, size_t smem, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+}  // namespace bm_wide
+
+namespace bm_wide {
+// the build's diagnostic phase counters (-DBM_DIAG=1 builds), added into out48
+cudaError_t add_phase_cycles(unsigned long long* out48, int reset) {
+  unsigned long long v[48];
+  cudaError_t e = cudaMemcpyFromSymbol(v, bmw::g_phase_cycles, 48 * 8);
+  if (e != cudaSuccess) return e;
+  for (int i = 0; i < 48; i++) out48[i] += v[i];
+  if (reset) {
+    unsigned long long z[48] = {0};
+    e = cudaMemcpyToSymbol(bmw::g_phase_cycles, z, 48 * 8);
+  }
+  return e;
+}
 }  // namespace bm_wide

@@ -14,6 +14,7 @@ constexpr int MAX_DEV = 64;
 struct DevState {
   int sms = 0;               // multiprocessor count
   int occ = 0;               // resident concealment CTAs per SM (256-thread build)
+  int clusters = 1;          // resident clusters of the cluster build
   std::atomic<bool> attr{false};       // k_conceal dynamic smem attribute
   std::atomic<bool> attr_w{false};     // 512-thread build
   std::atomic<bool> est_attr{false};   // k_estimate_batch

@@ -92,7 +92,43 @@ struct HqlSmem {
   int redidx[2][NWARP];
   int gbest;
   int fail;
+  double nearv[40];                      // the CTA's k-nearest distances (cluster merge)
+  double xb[CS > 1 ? 2 * 1024 : 1];      // DSMEM exchange, double-buffered (CS > 1)
 };
+
+constexpr int XB_HALF = 1024;
+
+// Cluster-wide fixed-order sum of warp 0's per-lane values v[0..N) (CS > 1):
+// each CTA publishes its partial in its exchange buffer, one cluster barrier,
+// then warp 0 of every CTA adds the CS partials in rank order over DSMEM, so
+// every CTA gets the same bits.  Called by all threads of every CTA; the
+// exchange buffer alternates (ph), so one barrier per exchange suffices.
+template <int N>
+__device__ __forceinline__ void cluster_sum_w0(double (&v)[N], HqlSmem& H, int& ph) {
+  static_assert(N * 32 <= XB_HALF, "exchange fits the buffer");
+  if constexpr (CS > 1) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* b = H.xb + ph * XB_HALF;
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < N; i++) b[i * 32 + lane] = v[i];
+    }
+    cluster_sync_all();
+    if (warp == 0) {
+      uint32_t base[CS];
+#pragma unroll
+      for (int r = 0; r < CS; r++) base[r] = map_rank(b, r) + lane * 8u;
+#pragma unroll
+      for (int i = 0; i < N; i++) {
+        double t = ld_dsmem_f64(base[0] + i * 256u);
+#pragma unroll
+        for (int r = 1; r < CS; r++) t += ld_dsmem_f64(base[r] + i * 256u);
+        v[i] = t;
+      }
+    }
+    ph ^= 1;
+  }
+}
 
 // per-CTA global scratch (doubles)
 constexpr size_t HQL_Z = 0;                                   // dense Z [MAXCAND][40] (estimator API only)
@@ -239,25 +275,29 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   long long ph_t = clock64();
   const int nks = (m + 3) >> 2;  // k-steps of 4 candidates
   const int nct = (m + 7) >> 3;  // column tiles of 8 candidates
+  // candidate loops run over the cluster's warps (CS = 1: this CTA's warps)
+  const unsigned rank = cluster_rank();
+  const int gw = (int)rank * NWARP + warp;
+  int xph = 0;  // exchange-buffer phase (cluster_sum_w0)
 
   // ---------------------------------------------------------------- means
   {
     // 4 independent accumulator pairs per lane (loads overlap), fixed-order combine
     double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
     const typename ZL::Ref c0 = zv.ref(H, lane), c1 = zv.ref(H, lane < 8 ? 32 + lane : 37);
-    int j = warp;
-    for (; j + 3 * NWARP < m; j += 4 * NWARP) {
+    int j = gw;
+    for (; j + 3 * GWARPS < m; j += 4 * GWARPS) {
 #pragma unroll
       for (int u = 0; u < 4; u++) {
-        const int b = zv.base(j + u * NWARP);
+        const int b = zv.base(j + u * GWARPS);
         a0[u] += zv.at(c0, b);
         a1[u] += zv.at(c1, b);
       }
     }
 #pragma unroll
-    for (int u = 0; u < 3; u++) {  // tail: j + 3 NWARP >= m
-      if (j + u * NWARP < m) {
-        const int b = zv.base(j + u * NWARP);
+    for (int u = 0; u < 3; u++) {  // tail: j + 3 GWARPS >= m
+      if (j + u * GWARPS < m) {
+        const int b = zv.base(j + u * GWARPS);
         a0[u] += zv.at(c0, b);
         a1[u] += zv.at(c1, b);
       }
@@ -267,11 +307,27 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     H.wmin[warp][lane] = a0[0];
     if (lane < 8) H.wmin[warp][32 + lane] = a1[0];
     __syncthreads();
-    if (tid < 40) {
-      double s = 0.0;
+    if constexpr (CS == 1) {
+      if (tid < 40) {
+        double s = 0.0;
 #pragma unroll
-      for (int w = 0; w < NWARP; w++) s += H.wmin[w][tid];
-      H.mean[tid] = s / m;  // z.mean(axis=0)
+        for (int w = 0; w < NWARP; w++) s += H.wmin[w][tid];
+        H.mean[tid] = s / m;  // z.mean(axis=0)
+      }
+    } else {
+      double v[2] = {0.0, 0.0};  // warp 0: columns lane and 32 + lane
+      if (warp == 0) {
+#pragma unroll
+        for (int w = 0; w < NWARP; w++) {
+          v[0] += H.wmin[w][lane];
+          if (lane < 8) v[1] += H.wmin[w][32 + lane];
+        }
+      }
+      cluster_sum_w0<2>(v, H, xph);
+      if (warp == 0) {
+        H.mean[lane] = v[0] / m;
+        if (lane < 8) H.mean[32 + lane] = v[1] / m;
+      }
     }
     __syncthreads();
     BM_PHASE(1);
@@ -308,10 +364,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         o[tl] = valid ? raw - mu[tl] : 0.0;
       }
     };
-    load_f(warp, f);
+    load_f(gw, f);
 #pragma unroll kCovUnroll
-    for (int s = warp; s < nks; s += NWARP) {
-      load_f(s + NWARP, fn);
+    for (int s = gw; s < nks; s += GWARPS) {
+      load_f(s + GWARPS, fn);
       int idx = 0;
 #pragma unroll
       for (int a = 0; a < 4; a++)
@@ -325,6 +381,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     }
     });
     tree_reduce<28, 14>(acc, H.R1);
+    cluster_sum_w0<28>(acc, H, xph);
     double* cyy = H.R1 + R1_SIZE - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
     double* L = cyy + 32 * 33;
     __syncwarp();
@@ -435,7 +492,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     } else {
       // warps 1..7: Euclidean distances in NumPy's order and the stable
       // k-nearest selection (optimize_alpha, estimators.py:221-223)
-      constexpr int NW7 = NT - 32, PER = (MAXCAND + NW7 - 1) / NW7;
+      // (CS > 1: this CTA takes the candidates j = l * CS + rank)
+      constexpr int NW7 = NT - 32, PER = (MAXCAND / CS + NW7 - 1) / NW7;
       const int t7 = tid - 32, w7 = warp - 1;
       double ev[PER];
       // dist2 = ((y - y0) ** 2).sum(axis=1) in NumPy's pairwise order: eight
@@ -452,7 +510,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
 #endif
       for (int i = 0; i < PER; i++) {
-        const int j = t7 + i * NW7;
+        const int j = (t7 + i * NW7) * CS + (int)rank;
 #if !BM_CNEAR
         ev[i] = INFINITY;
 #endif
@@ -483,7 +541,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #if BM_CNEAR
 #pragma unroll
       for (int i = 0; i < PER; i++) {
-        const int j = t7 + i * NW7;
+        const int j = (t7 + i * NW7) * CS + (int)rank;
         ev[i] = j < m ? dS[j] : INFINITY;
       }
 #endif
@@ -491,7 +549,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // (1) per-thread sort of its PER candidates by (e2, index)
       int ej[PER];
 #pragma unroll
-      for (int i = 0; i < PER; i++) ej[i] = t7 + i * NW7;
+      for (int i = 0; i < PER; i++) ej[i] = (t7 + i * NW7) * CS + (int)rank;
 #pragma unroll
       for (int pass = 0; pass < PER; pass++)
 #pragma unroll
@@ -535,14 +593,46 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           const double hv = (lane < NWARP - 1 && ptr < k) ? lv[lane * KMAX + ptr] : INFINITY;
           const int myj = (lane < NWARP - 1 && ptr < k) ? lj[lane * KMAX + ptr] : 0x7fffffff;
           int bj;
-          warp_argmin_key(hv, myj, bj);
-          if (lane == 0) H.near[it] = bj;
+          const double bv = warp_argmin_key(hv, myj, bj);
+          if (lane == 0) {
+            H.near[it] = bj;
+            H.nearv[it] = bv;
+          }
           if (myj == bj && lane < NWARP - 1) ptr++;
         }
         if (lane == 0) BM_DIAG_ADD(8, (clock64() - ph_t));  // nearest side (diagnostic)
       }
     }
     __syncthreads();
+    if constexpr (CS > 1) {
+      // the cluster's k nearest: merge the CS CTAs' sorted (distance, index)
+      // lists over DSMEM, identically in every CTA (ties -> smaller index)
+      const int k = min(n + 1, m);
+      double* b = H.xb + xph * XB_HALF;
+      if (tid < k) {
+        b[tid] = H.nearv[tid];
+        b[KMAX + tid] = (double)H.near[tid];
+      }
+      cluster_sync_all();
+      if (warp == 0) {
+        const uint32_t base = map_rank(b, lane < CS ? lane : 0);
+        int ptr = 0;
+        for (int it = 0; it < k; it++) {
+          double hv = INFINITY;
+          int hj = 0x7fffffff;
+          if (lane < CS && ptr < k) {
+            hv = ld_dsmem_f64(base + ptr * 8u);
+            hj = (int)ld_dsmem_f64(base + (KMAX + ptr) * 8u);
+          }
+          int bj;
+          warp_argmin_key(hv, hj, bj);
+          if (lane == 0) H.near[it] = bj;
+          if (lane < CS && hj == bj) ptr++;
+        }
+      }
+      xph ^= 1;
+      __syncthreads();
+    }
     BM_PHASE(3);
     if (H.fail) {
       if (tid == 0) out.ok = 0;
@@ -578,10 +668,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
       for (int kk = 0; kk < 8; kk++) o[kk] = kk < 2 * NA ? y0r[kk] - zv.at(ry[kk], bB) : 0.0;
     };
-    load_v(warp, fb);
+    load_v(gw, fb);
 #pragma unroll kQfUnroll
-    for (int c = warp; c < nct; c += NWARP) {
-      load_v(c + NWARP, fbn);
+    for (int c = gw; c < nct; c += GWARPS) {
+      load_v(c + GWARPS, fbn);
       double acc[8], acb[8];  // even / odd k-steps: two independent MMA chains
 #pragma unroll
       for (int i = 0; i < 8; i++) acc[i] = acb[i] = 0.0;
@@ -611,11 +701,20 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         const int col = 8 * c + 2 * t4;
         if (col < m) dS[col] = s0;
         if (col + 1 < m) dS[col + 1] = s1;
+        if constexpr (CS > 1) {  // every CTA of the cluster needs every d_j
+#pragma unroll
+          for (int r = 1; r < CS; r++) {
+            const unsigned peer = (rank + r) % CS;
+            if (col < m) st_dsmem_f64(map_rank(dS + col, peer), s0);
+            if (col + 1 < m) st_dsmem_f64(map_rank(dS + col + 1, peer), s1);
+          }
+        }
       }
     }
     });
   }
-  __syncthreads();
+  if constexpr (CS > 1) cluster_sync_all();
+  else __syncthreads();
   BM_PHASE(5);
   double dmin;
   {
@@ -658,10 +757,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       for (int ct = 0; ct < 5; ct++) o[ct] = (ct < NA || ct == 4) ? zv.at(crz[ct], b) : 0.0;  // weight 0 for padding
       if (g == ONES_COL - 32) o[4] = 1.0;
     };
-    load_b(warp, dl, fb);
+    load_b(gw, dl, fb);
 #pragma unroll kBetaUnroll
-    for (int s = warp; s < nks; s += NWARP) {
-      load_b(s + NWARP, dln, fbn);
+    for (int s = gw; s < nks; s += GWARPS) {
+      load_b(s + GWARPS, dln, fbn);
       double fa[3];
       const double e2w = brow ? exp_wn(dl * sc2, exptab) : 0.0;  // exp(expo - expo.max()); -inf -> 0
       fa[2] = e2w;
@@ -679,6 +778,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     });
     if (tid == 0) BM_DIAG_ADD(32, (clock64() - ph_t));  // beta loop (thread 0)
     tree_reduce<30, RED_CHUNK>(acc, H.R1);
+    cluster_sum_w0<30>(acc, H, xph);
     if (tid == 0) BM_DIAG_ADD(33, (clock64() - ph_t));  // beta loop + reduce
     constexpr int PS = 41;  // row stride of P: conflict-free per-lane row reads
     double* P = H.R2;       // [24][PS]
@@ -813,7 +913,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     with_na(n, [&](auto NAc) {
     constexpr int NA = decltype(NAc)::value;
 #pragma unroll kLooUnroll
-    for (int c = warp; c < nct; c += NWARP) {
+    for (int c = gw; c < nct; c += GWARPS) {
       // Gram B fragment of column tile c: (y0 - y_j)[4kk + t4] for j = 8c + g
       // (U vanishes beyond n: the padding dims' values only meet zeros)
       double fv[8];
@@ -880,11 +980,13 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     for (int rr = 0; rr < RR; rr++)
       if (t4 == 0) H.wmin[warp][rr * 8 + g] = xref[rr];
     __syncthreads();
+    double rowmx[RR];
 #pragma unroll
     for (int rr = 0; rr < RR; rr++) {
       double mx = -INFINITY;
 #pragma unroll
       for (int w = 0; w < NWARP; w++) mx = fmax(mx, H.wmin[w][rr * 8 + g]);
+      rowmx[rr] = mx;
       const double f = (xref[rr] == -INFINITY) ? 0.0 : exp(xref[rr] - mx);
 #pragma unroll
       for (int i = 0; i < 10; i++) acc[rr * 10 + i] *= f;
@@ -896,6 +998,38 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
       for (int i = 0; i < 10; i++) a10[i] = acc[rr * 10 + i];
       tree_reduce<10>(a10, H.R1);
+      if constexpr (CS > 1) {
+        // the CTAs' row sums are relative to their own row maxima: rescale to
+        // the cluster maximum and add in rank order (identical in every CTA)
+        double* b = H.xb + xph * XB_HALF;
+        if (warp == 0) {
+#pragma unroll
+          for (int i = 0; i < 10; i++) b[i * 32 + lane] = a10[i];
+          b[10 * 32 + lane] = rowmx[rr];
+        }
+        cluster_sync_all();
+        if (warp == 0) {
+          uint32_t base[CS];
+          double mr[CS], M = -INFINITY;
+#pragma unroll
+          for (int r = 0; r < CS; r++) {
+            base[r] = map_rank(b, r) + lane * 8u;
+            mr[r] = ld_dsmem_f64(base[r] + 10 * 256u);
+            M = fmax(M, mr[r]);
+          }
+          double f[CS];
+#pragma unroll
+          for (int r = 0; r < CS; r++) f[r] = mr[r] == -INFINITY ? 0.0 : exp(mr[r] - M);
+#pragma unroll
+          for (int i = 0; i < 10; i++) {
+            double t = ld_dsmem_f64(base[0] + i * 256u) * f[0];
+#pragma unroll
+            for (int r = 1; r < CS; r++) t += ld_dsmem_f64(base[r] + i * 256u) * f[r];
+            a10[i] = t;
+          }
+        }
+        xph ^= 1;
+      }
       const int row = 8 * (r0 + rr) + g;
       if (warp == 0 && row < KMAX) {
 #pragma unroll

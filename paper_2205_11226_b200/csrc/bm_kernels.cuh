@@ -3,10 +3,12 @@
 // dependency levels, ready FIFOs), the persistent CTA-per-lost-cell
 // concealment kernel and the dense estimator kernel.
 //
-// Compiled twice (namespace BM_NS, CTA width BM_NT): bm_conceal.cu (bm, 256
-// threads, 2 cells per SM) and bm_conceal_wide.cu (bmw, 512 threads, 1 cell
-// per SM) for dependency DAGs too narrow to fill 2 cells per SM, where the
-// per-cell latency (critical path) sets the time.
+// Compiled three times (namespace BM_NS, CTA width BM_NT, cluster size
+// BM_CS): bm_conceal.cu (bm, 256 threads, 2 cells per SM), bm_conceal_wide.cu
+// (bmw, 512 threads, 1 cell per SM) and bm_conceal_cluster.cu (bmc, 2-CTA
+// clusters of 512 threads per cell).  All three are launched; each returns at
+// once unless the dependency DAG's shape selects it (k_conceal): the narrower
+// the DAG, the more the per-cell latency (critical path) sets the time.
 #pragma once
 #include "../../include/blockmend_b200.h"
 #include "bm_common.cuh"
@@ -41,10 +43,12 @@ struct KParams {
   double* scratch;     // per-CTA HQL scratch
   size_t scratch_per_cta;  // doubles
   int sms;             // SM count (narrow-DAG test)
-  int build;           // 0: by DAG shape; 256 / 512: force that kernel build
+  int build;           // 0: by DAG shape; 256 / 512 / BUILD_CLUSTER: force that kernel build
+  int narrow_cluster;  // narrow DAGs: 1 = the cluster build, 0 = the 512-thread build
   int* ringtab;        // [64][33]: interior cells' expansion-map ring offsets per patch position + max ring
 };
 
+constexpr int BUILD_CLUSTER = 1024;  // KParams::build code of the cluster build
 constexpr int GH = 2, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
 #ifndef BM_FIRST_GH
 #define BM_FIRST_GH 1
@@ -637,7 +641,7 @@ __device__ __forceinline__ unsigned long long hql_flops(long long M, long long n
 }
 
 __device__ void write_record(const KParams& P, CellSmem& S, const bm_patch_record& rec) {
-  if (P.records) P.records[(size_t)S.slot * 64 + S.nrec] = rec;
+  if (P.records && cluster_rank() == 0) P.records[(size_t)S.slot * 64 + S.nrec] = rec;
 }
 
 // One patch at tile position (pr_t, pc_t): gate + estimate
@@ -921,6 +925,7 @@ __device__ void pick_and_extract(CellSmem& S) {
   }
 }
 
+#ifndef BM_CONCEAL_ONLY  // the library-API kernels: the 256-thread translation unit only
 // A TargetContext supplied by the caller (the per-patch library API,
 // framework.py:60-77): usable bits over CONTEXT_OFFSETS and y0 in layout
 // order, instead of pick_and_extract's extraction.  Warp 0.
@@ -996,6 +1001,8 @@ __global__ void __launch_bounds__(NT, 1) k_select(KParams P, SelectArgs A) {
   }
 }
 
+#endif  // BM_CONCEAL_ONLY
+
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   CellSmem& S = *reinterpret_cast<CellSmem*>(smem_raw);
@@ -1005,23 +1012,42 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
   init_exptab(S.est);
   if (tid == 0) S.idl_diag = 0;
   const int nslots = *((volatile int*)P.nslots);
-  // Narrow dependency DAGs (few cells, or long chains: average width
-  // cells / levels below the 2 x SMs cell slots of the 256-thread build) are
-  // latency-bound on their critical path: the 512-thread build (one cell per
-  // SM, twice the warps per cell) runs them, the other build steps aside.
+  // Build choice (identical in every CTA of the three launched builds): by
+  // the dependency DAG's average width W = lost cells / levels against each
+  // build's concurrent cells (256-thread: 2 per SM, 512-thread: 1 per SM,
+  // cluster: 1 per 2 SMs) and the workload's weight.  Narrow DAGs are
+  // latency-bound on their critical path, where fewer, faster cell workers
+  // win; all-HQL work is heavy enough to stay throughput-bound at smaller W.
+  // Thresholds measured on cfg1-cfg5 and cfg5 shards of 16..256 frames
+  // (profiles/scale_sim_r02.txt).
   {
-    const unsigned long long levels = P.counters[7] + 1;
-    const bool narrow = P.build ? P.build == 512 : (unsigned long long)nslots < levels * 2ull * (unsigned long long)P.sms;
-    if (narrow != (NT > 256)) return;
+    const double levels = (double)(P.counters[7] + 1);
+    const double w = (double)nslots / levels * (148.0 / (double)P.sms);
+    const bool all_hql = P.forced == BM_LAYER_HQL || (P.forced < 0 && P.t_phi < 0.0 && isinf(P.t_nu));
+    const bool gated = P.forced < 0 && !all_hql;
+    const double w_cluster = gated ? 450.0 : 96.0, w_512 = gated ? 1000.0 : 192.0;
+    int want = w <= w_cluster ? (P.narrow_cluster ? BUILD_CLUSTER : 512) : (w <= w_512 ? 512 : 256);
+    if (P.build) want = P.build;
+    const int mine = NT <= 256 ? 256 : (CS > 1 ? BUILD_CLUSTER : 512);
+    if (mine != want) return;
   }
+  const unsigned crank = cluster_rank();
   const long long t_cta0 = clock64();
   for (;;) {
     const long long t_w0 = clock64();
-    if (tid < 32) {
+    if (crank == 0 && tid < 32) {
       const int slot = sched_pop(P, nslots);
       if (tid == 0) S.slot = slot;
     }
-    __syncthreads();
+    if constexpr (CS > 1) {
+      // rank 0 pops; the cluster's other CTAs take the same cell (the acquire
+      // chain: rank 0's queue acquire, then the cluster barrier's)
+      cluster_sync_all();
+      if (crank != 0 && tid == 0) S.slot = ld_dsmem_s32(map_rank(&S.slot, 0));
+      cluster_sync_all();  // rank 0 pops again only after every peer has read
+    } else {
+      __syncthreads();
+    }
     if (S.slot < 0) break;
     if (tid == 0) {
       const int slot = S.slot;
@@ -1116,8 +1142,9 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
       }
     }
     __syncthreads();
-    // publish the cell (values, outputs), then release the flag
-    {
+    // publish the cell (values, outputs), then release the flag (cluster
+    // build: rank 0; the other CTAs hold the same values)
+    if (crank == 0) {
       const size_t slot = S.slot;
       const int f = S.f;
       const int r0 = S.gr * BS, c0 = S.gc * BS;
@@ -1151,8 +1178,10 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
     BM_DIAG_ADD(22, (clock64() - t_cta0));  // CTA lifetime
     BM_DIAG_ADD(23, 1);
   }
-  if (tid < 4 && S.cnt[tid]) atomicAdd(&P.counters[tid], S.cnt[tid]);
-  if (tid >= 4 && tid < 8 && S.cnt[tid]) atomicAdd(&P.counters[tid + 4], S.cnt[tid]);
+  if (crank == 0) {  // (cluster build: every CTA counted the same cells)
+    if (tid < 4 && S.cnt[tid]) atomicAdd(&P.counters[tid], S.cnt[tid]);
+    if (tid >= 4 && tid < 8 && S.cnt[tid]) atomicAdd(&P.counters[tid + 4], S.cnt[tid]);
+  }
 }
 
 // Dense output initialisation: out_f64 = pixels, out_u8 = quantized(pixels).
@@ -1185,6 +1214,7 @@ __global__ void k_summary(KParams P, bm_summary* out) {
 }
 
 // ------------------------------------------------------- dense estimator API
+#ifndef BM_CONCEAL_ONLY
 
 struct EstBatchArgs {
   int layer, count, max_m;
@@ -1276,6 +1306,8 @@ __global__ void __launch_bounds__(NT, 1) k_estimate_batch(EstBatchArgs A) {
     for (int q = 0; q < 4; q++) A.out_values[(size_t)i * 4 + q] = E.vals[q];
   }
 }
+
+#endif  // BM_CONCEAL_ONLY
 
 __global__ void k_compact_records(const bm_patch_record* slot_rec, const uint8_t* cnt, const int* excl,
                                   const int* nslots, bm_patch_record* out) {

@@ -176,8 +176,10 @@ def conceal_batch(
     [B,H,W] (cuda, values in {0,1,2}).  Runs asynchronously on torch's current
     stream; with sync=True the summary is read back (raising the reference's
     errors for leftover LOST pixels / bad states).  kernel_build: None picks
-    the CTA width from the dependency DAG's shape; 256 or 512 forces one
-    (both meet the parity bar; their results can differ in the last bits).
+    the build from the dependency DAG's shape; 256, 512 or 'cluster' (2-CTA
+    clusters of 512 threads per cell) forces one, 'narrow512' keeps the
+    512-thread build for narrow DAGs (all meet the parity bar; their FP64
+    reduction orders differ, so results can differ in the last bits).
     """
     torch = _native.require_cuda()
     if frames.dim() == 2:
@@ -203,9 +205,11 @@ def conceal_batch(
     if time_kernel:
         params.flags |= _native.BM_FLAG_TIME_KERNEL
     if kernel_build is not None:
-        if kernel_build not in (256, 512):
-            raise ValueError("kernel_build must be None, 256 or 512")
-        params.flags |= _native.BM_FLAG_BUILD_256 if kernel_build == 256 else _native.BM_FLAG_BUILD_512
+        flag = {256: _native.BM_FLAG_BUILD_256, 512: _native.BM_FLAG_BUILD_512,
+                "cluster": _native.BM_FLAG_BUILD_CLUSTER, "narrow512": _native.BM_FLAG_NARROW_512}.get(kernel_build)
+        if flag is None:
+            raise ValueError("kernel_build must be None, 256, 512, 'cluster' or 'narrow512'")
+        params.flags |= flag
     dev = frames.device
     with torch.cuda.device(dev):  # the C ABI works on the current device
         nbytes, ws, summ_buf, rec, rec2 = _workspace(torch, params, dev, records)

@@ -7,13 +7,16 @@ from paper_2205_11226_b200 import _native
 from paper_2205_11226_b200.profiles import conceal_batch
 from paper_2205_11226_b200.synth import make_config
 cfg = int(sys.argv[1]); nf = int(sys.argv[2]); prof = sys.argv[3]
+kb = sys.argv[4] if len(sys.argv) > 4 else None
+kb = None if kb is None else (int(kb) if kb.isdigit() else kb)
+per_cta = 2 if kb == "cluster" else 1  # the cluster build's CTAs each count every phase
 px, st = make_config(cfg, frames=nf)
 p = bm.Profile.sentinel() if prof == 'sentinel' else bm.Profile.named(prof)
 tp, ts = torch.from_numpy(px).cuda(), torch.from_numpy(st).cuda()
-conceal_batch(tp, ts, p)
+conceal_batch(tp, ts, p, kernel_build=kb)
 _native.phase_cycles(reset=True)
-r = conceal_batch(tp, ts, p, time_kernel=True)
-ph = _native.phase_cycles(reset=True)
+r = conceal_batch(tp, ts, p, time_kernel=True, kernel_build=kb)
+ph = {k: v // per_cta for k, v in _native.phase_cycles(reset=True).items()}
 n_hql = r.summary['hql_patches']
 tot = sum(v for k, v in ph.items() if not k.startswith('patch'))
 print('kernel ms', _native.kernel_times_ms()[-1], 'hql patches', n_hql, r.summary['layer_counts'])

@@ -16,7 +16,7 @@ px_all, st_all = make_config(5, frames=max(frames))
 for nf in frames:
     tp = torch.from_numpy(px_all[:nf]).cuda()
     ts = torch.from_numpy(st_all[:nf]).cuda()
-    for build in (None, 256, 512):
+    for build in (None, 256, 512, "cluster"):
         conceal_batch(tp, ts, prof, kernel_build=build)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ms = []
@@ -27,4 +27,4 @@ for nf in frames:
             e1.synchronize()
             ms.append(e0.elapsed_time(e1))
         cells = r.summary["lost_cells"] if r.summary else 0
-        print(f"frames {nf:4d} build {str(build):4s}: {min(ms):8.1f} ms  ({cells / (min(ms) / 1e3):9.0f} cells/s per GPU)", flush=True)
+        print(f"frames {nf:4d} build {str(build):7s}: {min(ms):8.1f} ms  ({cells / (min(ms) / 1e3):9.0f} cells/s per GPU)", flush=True)
