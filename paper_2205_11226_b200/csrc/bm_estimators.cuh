@@ -23,7 +23,9 @@ struct TileAcc {
   const double* tile;     // smem [TILE*TS]
   const uint16_t* cand;   // smem window-origin tile positions
   const int16_t* uoff;    // smem used offsets: n context then 4 patch cells
+  const float* tile32;    // smem FP32 shadow of the tile (BM_IDL_FP32 experiment)
   __device__ __forceinline__ double y(int j, int t) const { return tile[cand[j] + uoff[t]]; }
+  __device__ __forceinline__ float yf(int j, int t) const { return tile32[cand[j] + uoff[t]]; }
   __device__ __forceinline__ double x(int j, int q) const {
     return tile[cand[j] + (2 + (q >> 1)) * TS + 2 + (q & 1)];
   }
@@ -33,6 +35,7 @@ struct DenseAcc {
   const double* X;  // [m][4]   (global)
   const double* Y;  // [m][32]  (global)
   __device__ __forceinline__ double y(int j, int t) const { return Y[(size_t)j * 32 + t]; }
+  __device__ __forceinline__ float yf(int j, int t) const { return (float)Y[(size_t)j * 32 + t]; }
   __device__ __forceinline__ double x(int j, int q) const { return X[(size_t)j * 4 + q]; }
 };
 
@@ -126,6 +129,84 @@ __device__ __forceinline__ void brl_values(EstSmem& S) {
 // (exbuf, >= m doubles).  Called from one site per kernel (one inlined copy:
 // instruction-cache footprint).
 // Sets S.ok = 0 on WeightUnderflowError (raw_sum == 0); S.nu_raw = raw_sum.
+#ifndef BM_IDL_FP32
+#define BM_IDL_FP32 0
+#endif
+#if BM_IDL_FP32
+// EXPERIMENT (tools/fp32_idl.sh; not the product build): the
+// north_star's FP32 Nadaraya-Watson weighting inside the IDL estimate -
+// FP32 distances (fmaf over the FP32 tile shadow), FP32 exponents and expf
+// weights, FP64 accumulation of the weighted sums and normalisation, and the
+// reference's FP64 underflow predicate (raw_sum == 0) evaluated from the
+// largest exponent in the log domain.
+template <class Acc>
+__device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf,
+                                                 bool want_raw, bool final_sync = true) {
+  const int n = S.n, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const float invc = (float)(1.0 / (2.0 * sigma2 * n));
+  float* ef = reinterpret_cast<float*>(exbuf);
+  float emax = -INFINITY;
+#pragma unroll 1
+  for (int j = threadIdx.x; j < m; j += NT) {
+    float d2a = 0.f, d2b = 0.f;
+    int t = 0;
+#pragma unroll 1
+    for (; t + 2 <= n; t += 2) {
+      const float da = acc.yf(j, t) - S.y0f[t], db = acc.yf(j, t + 1) - S.y0f[t + 1];
+      d2a = fmaf(da, da, d2a);
+      d2b = fmaf(db, db, d2b);
+    }
+    if (t < n) {
+      const float da = acc.yf(j, t) - S.y0f[t];
+      d2a = fmaf(da, da, d2a);
+    }
+    const float e = -(d2a + d2b) * invc;
+    ef[j] = e;
+    emax = fmaxf(emax, e);
+  }
+  emax = warp_minf(-emax) * -1.f;  // warp max
+  if (lane == 0) S.redf[warp] = emax;
+  __syncthreads();
+  emax = S.redf[0];
+#pragma unroll
+  for (int w = 1; w < NWARP; w++) emax = fmaxf(emax, S.redf[w]);
+  double v5[5] = {0, 0, 0, 0, 0};
+#pragma unroll 1
+  for (int j = threadIdx.x; j < m; j += NT) {
+    const double sh = (double)__expf(ef[j] - emax);
+    v5[0] += sh;
+#pragma unroll
+    for (int q = 0; q < 4; q++) v5[1 + q] = fma(sh, acc.x(j, q), v5[1 + q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 5; q++) v5[q] = warp_sum(v5[q]);
+  if (lane == 0) {
+#pragma unroll
+    for (int q = 0; q < 5; q++) S.red[warp][q] = v5[q];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+    if (lane < 5) {
+      t = S.red[0][lane];
+#pragma unroll
+      for (int w = 1; w < NWARP; w++) t += S.red[w][lane];
+    }
+    const double t0 = __shfl_sync(FULL, t, 0);
+    if (lane >= 1 && lane < 5) S.vals[lane - 1] = t * (1.0 / t0);
+    if (lane == 0) {
+      if (want_raw) {
+        const double e0 = exp((double)emax);  // log-domain FP64 underflow predicate
+        S.nu_raw = e0 * t0;
+        S.ok = e0 != 0.0;
+      } else {
+        S.ok = 1;
+      }
+    }
+  }
+  if (final_sync) __syncthreads();
+}
+#else
 template <class Acc>
 __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double sigma2, EstSmem& S, double* exbuf,
                                                  bool want_raw, bool final_sync = true) {
@@ -206,5 +287,6 @@ __device__ __forceinline__ void idl_estimate_dev(const Acc& acc, int m, double s
   }
   if (final_sync) __syncthreads();
 }
+#endif  // BM_IDL_FP32
 
 }  // namespace BM_NS

@@ -688,7 +688,7 @@ __device__ void estimate_only(const KParams& P, CellSmem& S, int pr_t, int pc_t,
       S.cnt[5] += (unsigned long long)m * (3 * E.n + 2);
       S.cnt[7] += (unsigned long long)m;
     }
-    TileAcc acc{S.tile, S.cand, E.uoff};
+    TileAcc acc{S.tile, S.cand, E.uoff, S.tile32};
     if (tid == 0) {
       rec.rings_used = (uint8_t)S.rings_used;
       rec.m_candidates = m;
