@@ -38,9 +38,9 @@ UNIT = "blocks/s"
 # 36.8 TF/s DMMA, 36.2 DFMA (profiles/peaks_r01.txt) -> the roofline uses 36.8.
 FP64_PEAK_TFLOPS = 36.8
 FP32_PEAK_TFLOPS = 69.7  # measured FFMA peak (same run)
-LAUNCHES_PER_STEP = 12   # k_init_out, k_cell_flags, 2 x CUB scan, k_slots, 2 x k_depth, k_sched_prep,
-                         # k_sched_seed, k_conceal (256- and 512-thread builds; the one not serving
-                         # the DAG shape returns at once), k_summary (profiles/ launch list)
+LAUNCHES_PER_STEP = 14   # k_init_out, k_cell_flags, 2 x CUB scan, k_slots, 2 x k_depth, k_sched_prep, k_postab,
+                         # k_sched_seed, k_conceal x 3 (256-thread, 512-thread and 2-CTA cluster builds; the
+                         # two not serving the DAG shape return at once), k_summary (profiles/ launch list)
 TRAFFIC_FILE = os.path.join(ROOT, "profiles", "ncu_traffic.json")  # ncu --set full dram bytes per launch
 
 WORKLOADS = {

@@ -63,7 +63,8 @@ constexpr int NARROW_CLUSTER_DEFAULT = 1;
 struct Layout {
   size_t ncell;
   size_t off_slotmap, off_slot_cell, off_level, off_level2, off_height, off_bucket, off_queue, off_indeg, off_nslots,
-      off_sched, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_ringtab, off_cub, cub_bytes, off_scratch,
+      off_sched, off_flags, off_excl, off_cellbuf, off_reccnt, off_counters, off_ringtab, off_postab, off_cub, cub_bytes,
+      off_scratch,
       scratch_per_cta, total;
   int grid;
 };
@@ -121,6 +122,7 @@ Layout layout(const bm_params* p) {
   L.off_reccnt = o; o = align_up(o + nc);
   L.off_counters = o; o = align_up(o + 16 * 8);
   L.off_ringtab = o; o = align_up(o + 64 * 33 * 4);
+  L.off_postab = o; o = align_up(o + 64 * MAXCAND * 2);
   size_t b1 = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, b1, (int*)nullptr, (int*)nullptr, (int)nc);
   L.cub_bytes = b1;
@@ -248,6 +250,7 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
   P.rec_count = (uint8_t*)(ws + L.off_reccnt);
   P.counters = (unsigned long long*)(ws + L.off_counters);
   P.ringtab = (int*)(ws + L.off_ringtab);
+  P.postab = (uint16_t*)(ws + L.off_postab);
   P.scratch = (double*)(ws + L.off_scratch);
   P.scratch_per_cta = L.scratch_per_cta;
   P.sms = sm_count();
@@ -277,6 +280,7 @@ int bm_conceal(const bm_params* p, const void* pixels, const uint8_t* states, do
     // dataflow scheduler: dependency counters, priority buckets, ready FIFOs
     if ((e = cudaMemsetAsync(P.queue, 0xFF, (size_t)nc * 4, stream)) != cudaSuccess) return cuda_status(e);
     k_sched_prep<<<sms, 256, 0, stream>>>(P, height);
+    k_postab<<<64, 256, 0, stream>>>(P);
     k_sched_seed<<<sms, 256, 0, stream>>>(P);
     const size_t smem = sizeof(CellSmem), smem_w = bm_wide::cell_smem_bytes();
     bm_host::DevState& D = bm_host::dev_state();

@@ -46,6 +46,8 @@ struct KParams {
   int build;           // 0: by DAG shape; 256 / 512 / BUILD_CLUSTER: force that kernel build
   int narrow_cluster;  // narrow DAGs: 1 = the cluster build, 0 = the 512-thread build
   int* ringtab;        // [64][33]: interior cells' expansion-map ring offsets per patch position + max ring
+  uint16_t* postab;    // [64][MAXCAND]: interior cells' expansion map per patch position: window
+                       // origin (tile row << 8 | tile col) of every entry, in (ring, row, col) order
 };
 
 constexpr int BUILD_CLUSTER = 1024;  // KParams::build code of the cluster build
@@ -284,6 +286,41 @@ __global__ void k_sched_prep(KParams P, const unsigned* height) {
   }
 }
 
+// The expansion map of an interior cell's 64 patch positions (window
+// origins in tile coordinates; translation invariant, like ringtab), so the
+// gate's screening reads an entry's window from a table instead of solving
+// the ring / raster position in closed form.  One CTA per patch position.
+__global__ void k_postab(KParams P) {
+  __shared__ int off[32];
+  const int p = blockIdx.x, tid = threadIdx.x;
+  RingGeom g;
+  g.pr = BS + 2 * (p >> 3);
+  g.pc = BS + 2 * (p & 7);
+  g.A0 = 2;
+  g.A1 = TILE - 4;
+  g.B0 = 2;
+  g.B1 = TILE - 4;
+  if (tid < 32) {
+    const int cnt = (tid >= 1 && tid <= 28) ? ring_count(g, tid) : 0;
+    int inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(FULL, inc, o);
+      inc += tid >= o ? v : 0;
+    }
+    off[tid] = inc - cnt;
+  }
+  __syncthreads();
+  const int K = off[31];
+  for (int e = tid; e < K; e += blockDim.x) {
+    int r = 1;
+    while (r < 31 && off[r + 1] <= e) r++;
+    int a, b;
+    ring_entry(g, r, e - off[r], a, b);
+    P.postab[(size_t)p * MAXCAND + e] = (uint16_t)(((a - 2) << 8) | (b - 2));
+  }
+}
+
 // bucket offsets (every block computes them; block 0 publishes) and the
 // initially ready cells (no lost earlier-raster neighbour)
 __global__ void k_sched_seed(KParams P) {
@@ -422,7 +459,8 @@ __device__ __forceinline__ float nu_weight(const CellSmem& S, int pos, int n, fl
 }
 
 __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int e0, int gh, int K, int max_ring,
-                                            int R0, int C0, bool gated, float invf, int m0, bool sync_end) {
+                                            int R0, int C0, bool gated, float invf, int m0, bool sync_end,
+                                            const uint16_t* __restrict__ tab) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   EstSmem& E = S.est;
   const int n = E.n;
@@ -437,12 +475,20 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
       // ring of entry e: the last ring starting at or before e (empty rings
       // share their successor's offset), branch-free binary search over the
       // 32 ring offsets (rings past max_ring start at K > e)
-      int lo = 0;
+      int wr, wc;  // window origin, tile coords
+      if (tab) {     // interior cell: the precomputed expansion map (k_postab)
+        const unsigned v = __ldg(tab + e);
+        wr = (int)(v >> 8);
+        wc = (int)(v & 255u);
+      } else {
+        int lo = 0;
 #pragma unroll
-      for (int step = 16; step; step >>= 1) lo += S.ring_off[lo + step] <= e ? step : 0;
-      int a, b;
-      ring_entry(g, lo, e - S.ring_off[lo], a, b);
-      const int wr = a - 2 - R0, wc = b - 2 - C0;  // window origin, tile coords
+        for (int step = 16; step; step >>= 1) lo += S.ring_off[lo + step] <= e ? step : 0;
+        int a, b;
+        ring_entry(g, lo, e - S.ring_off[lo], a, b);
+        wr = a - 2 - R0;
+        wc = b - 2 - C0;
+      }
       bool ok = true;
 #pragma unroll
       for (int q = 0; q < 6; q++)
@@ -552,6 +598,11 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     return;
   }
   const float invf = (float)(1.0 / (2.0 * P.sigma2 * n));
+  // interior cells at schedule positions: the expansion map from the table
+  const bool interior = r0 == br - BS && c0 == bc - BS && r1 == br + 2 * BS && c1 == bc + 2 * BS;
+  const uint16_t* tab = (P.postab && P.ringtab && ((pr_t | pc_t) & 1) == 0 && interior)
+                            ? P.postab + (size_t)((pr_t - BS) / 2 * 8 + (pc_t - BS) / 2) * MAXCAND
+                            : nullptr;
   // one screening loop (a single inlined copy of screen_chunk): ungated = the
   // whole map; gated = the first chunk, its ring-by-ring nu stop, then the
   // rest of the map in one sweep.  The nu accounting (per-ring sums, one warp
@@ -564,7 +615,7 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
   for (int e0 = 0; e0 < K; e0 += (e0 == 0 ? gh1 : GH) * NT) {
     const int gh = e0 == 0 ? gh1 : GH;
     const bool acct = gated && (e0 == 0 || e0 + gh * NT >= K);  // nu accounting after this chunk
-    mtot += screen_chunk(S, g, e0, gh, K, max_ring, R0, C0, gated, invf, mtot, !acct);
+    mtot += screen_chunk(S, g, e0, gh, K, max_ring, R0, C0, gated, invf, mtot, !acct, tab);
     if (!acct) continue;
     const int elo = e0 == 0 ? 0 : e1, ehi = e0 == 0 ? e1 : K;
     const int rs = e0 == 0 ? 1 : S.cur_ring;  // first ring not yet accounted (may carry a partial sum)
