@@ -387,10 +387,74 @@ __device__ int sched_pop(const KParams& P, int nslots) {
 
 // --------------------------------------------------------- the cell kernel
 
+// Stage the cell's 48x48 support tile: FP64 values, FP32 shadow, states and
+// the per-row LOST / AVAILABLE bitmaps.  Interior tiles of u8 frames take the
+// vector path: one thread per (tile row, 16-column chunk) - each chunk lies
+// inside one neighbouring cell - moves 16 pixels and 16 states with two
+// 16-byte loads (or, for a finished earlier-raster neighbour, its 16 final
+// FP64 values from the cell buffer with eight 16-byte loads) and builds the
+// chunk's 16-bit LOST / AVAILABLE masks on the way.
 __device__ void load_tile(const KParams& P, CellSmem& S) {
   const int f = S.f, gr = S.gr, gc = S.gc;
   const int R0 = gr * BS - BS, C0 = gc * BS - BS;
   const int H = P.H, W = P.W;
+  const bool vec = !P.pix_f64 && (W & 15) == 0 && R0 >= 0 && R0 + TILE <= H && C0 >= 0 && C0 + TILE <= W &&
+                   ((reinterpret_cast<uintptr_t>(P.pixels) | reinterpret_cast<uintptr_t>(P.states)) & 15) == 0;
+  if (vec) {
+    __shared__ uint16_t lmask[TILE * 3], amask[TILE * 3];
+    for (int t = threadIdx.x; t < TILE * 3; t += NT) {
+      const int tr = t / 3, ch = t % 3;  // tile row, 16-column chunk (= neighbour column ch)
+      const size_t o = ((size_t)f * H + R0 + tr) * W + C0 + 16 * ch;
+      const uint4 sv = __ldg(reinterpret_cast<const uint4*>(P.states + o));
+      const int ntr = tr / BS;
+      int pslot = -1;
+      if (P.slotmap && (ntr == 0 || (ntr == 1 && ch == 0)))
+        pslot = P.slotmap[((size_t)f * P.GR + gr - 1 + ntr) * P.GC + gc - 1 + ch];
+      const uint8_t* sb = reinterpret_cast<const uint8_t*>(&sv);
+      double* trow = S.tile + tr * TS + 16 * ch;
+      float* frow = S.tile32 + tr * TS + 16 * ch;
+      uint8_t* srow = S.st + tr * TS + 16 * ch;
+      unsigned lm = 0, am = 0;
+      if (pslot >= 0) {  // finished earlier-raster neighbour: its final values, LOST -> RECONSTRUCTED
+        const double2* cb = reinterpret_cast<const double2*>(P.cellbuf + (size_t)pslot * 256 + (tr % BS) * BS);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const double2 v = __ldcg(cb + q);
+          trow[2 * q] = v.x;
+          trow[2 * q + 1] = v.y;
+          frow[2 * q] = (float)v.x;
+          frow[2 * q + 1] = (float)v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          const uint8_t st = sb[q] == ST_LO ? ST_RE : sb[q];
+          srow[q] = st;
+          am |= (unsigned)(st == ST_AV) << q;
+        }
+      } else {
+        const uint4 pv = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(P.pixels) + o));
+        const uint8_t* pb = reinterpret_cast<const uint8_t*>(&pv);
+#pragma unroll
+        for (int q = 0; q < 16; q++) {
+          trow[q] = (double)pb[q];
+          frow[q] = (float)pb[q];
+          srow[q] = sb[q];
+          lm |= (unsigned)(sb[q] == ST_LO) << q;
+          am |= (unsigned)(sb[q] == ST_AV) << q;
+        }
+      }
+      lmask[t] = (uint16_t)lm;
+      amask[t] = (uint16_t)am;
+    }
+    __syncthreads();
+    if (threadIdx.x < TILE) {
+      const int r = threadIdx.x;
+      S.lostbits[r] = (uint64_t)lmask[3 * r] | ((uint64_t)lmask[3 * r + 1] << 16) | ((uint64_t)lmask[3 * r + 2] << 32);
+      S.availbits[r] = (uint64_t)amask[3 * r] | ((uint64_t)amask[3 * r + 1] << 16) | ((uint64_t)amask[3 * r + 2] << 32);
+    }
+    __syncthreads();
+    return;
+  }
   for (int i = threadIdx.x; i < TILE * TILE; i += NT) {
     const int tr = i / TILE, tc = i % TILE;
     const int r = R0 + tr, c = C0 + tc;
