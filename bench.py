@@ -31,6 +31,8 @@ sys.path.insert(0, ROOT)
 
 from paper_2205_11226_b200.synth import CONFIGS, make_config  # noqa: E402
 
+BUILD_LABEL = {"256": "256-thread CTAs, 2 cells/SM", "512": "512-thread CTAs, 1 cell/SM (narrow DAG)",
+               "cluster": "2-CTA clusters of 512 threads per cell (narrow DAG)"}
 METRIC = "lost 16x16 blocks concealed/sec"
 UNIT = "blocks/s"
 # FP64 peak: DMMA (mma.sync m8n8k4 f64) and DFMA share the SM's FP64 hardware
@@ -547,9 +549,7 @@ def main():
                        "parallelism": (f"frames sharded x{world} (strong)" if scaling == "strong" else
                                        f"{n_frames} frames per rank x{world}" if n_frames > 1 else f"replicas x{world}"),
                        "result_gather": "dist.gather of the u8 frames to rank 0 (NCCL), preallocated buffers",
-                       "conceal_build": ("512-thread CTAs, 1 cell/SM (narrow DAG)"
-                                         if summ["lost_cells"] < (summ["max_level"] + 1) * 2 * sms
-                                         else "256-thread CTAs, 2 cells/SM")},
+                       "conceal_build": BUILD_LABEL.get(summ.get("kernel_build"), summ.get("kernel_build"))},
             "gpu_launches": LAUNCHES_PER_STEP * args.steps if cuda else 0,
             "roofline": roof,
             "cpu_baseline": cpu,

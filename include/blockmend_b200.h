@@ -100,6 +100,8 @@ typedef struct bm_summary {
   int64_t flop32;         /* FP32: nu-gate distance/weight screening */
   int64_t hql_patches;    /* patches that ran the full HQL pipeline */
   int64_t gate_candidates;/* candidates screened by the FP32 nu gate */
+  int32_t kernel_build;   /* the concealment build that ran: 256, 512 or 1024 (2-CTA clusters); 0 = none */
+  int32_t reserved;
 } bm_summary;
 
 /* bm_params.flags */

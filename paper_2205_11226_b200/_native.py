@@ -59,6 +59,8 @@ class Summary(ctypes.Structure):
         ("flop32", ctypes.c_int64),
         ("hql_patches", ctypes.c_int64),
         ("gate_candidates", ctypes.c_int64),
+        ("kernel_build", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

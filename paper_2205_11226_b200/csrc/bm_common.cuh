@@ -322,6 +322,27 @@ __device__ __forceinline__ double exp_wn(double a, const double* __restrict__ ta
   const double res = __hiloint2double(__double2hiint(v) + ((ki >> 6) << 20), __double2loint(v));  // * 2^(ki>>6)
   return a >= -708.0 ? res : 0.0;
 }
+// exp_wn without the FP64 compares: the argument clamp and the underflow test
+// run on the integer pipe (the rounded exponent k = round(a 64/ln2) is the
+// 64-bit difference of t and the shifter, exact while |k| < 2^51); k below
+// -1021*64 (a < ~-707.6) -> 0, and so are a = -inf and any a < -2^44.  For
+// a <= 25 or -inf; a = +inf / NaN give garbage (callers select them away).
+__device__ __forceinline__ double exp_wf(double a, const double* __restrict__ tab) {
+  const double t = fma(a, c_expw[0], 0x1.8p52);
+  const long long kb = __double_as_longlong(t) - 0x4338000000000000ll;
+  const int ki = (int)kb;
+  const double kd = t - 0x1.8p52;
+  double r = fma(kd, -c_expw[1], a);
+  r = fma(kd, -c_expw[2], r);
+  const double r2 = r * r;
+  const double p23 = fma(r, c_expw[3], 0.5);
+  const double p45 = fma(r, c_expw[4], c_expw[5]);
+  const double q = fma(r2, fma(r2, p45, p23), r);  // e^r - 1
+  const double2 tj = reinterpret_cast<const double2*>(tab)[ki & 63];
+  const double v = tj.x + fma(tj.x, q, tj.y);
+  const double res = __hiloint2double(__double2hiint(v) + ((ki >> 6) << 20), __double2loint(v));
+  return kb >= -1021ll * 64 ? res : 0.0;
+}
 // general version: NaN stays NaN, overflow -> inf
 __device__ __forceinline__ double exp_w(double a, const double* __restrict__ tab) {
   const double res = exp_wn(a, tab);

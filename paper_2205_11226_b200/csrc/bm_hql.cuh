@@ -62,6 +62,15 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)
 constexpr int kBetaUnroll = BM_BETA_UNROLL, kCovUnroll = BM_COV_UNROLL, kQfUnroll = BM_QF_UNROLL,
               kLooUnroll = BM_LOO_UNROLL;
 constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (36 = 4 mod 16)
+#ifndef BM_LOO_FAST
+#define BM_LOO_FAST 1  // LOO / beta weights: integer-pipe exp underflow and clamp, fused x - xref (A/B)
+#endif
+#ifndef BM_COV1P
+#define BM_COV1P 0  // one-pass covariance about a sampled shift (no means pass) (A/B)
+#endif
+#ifndef BM_LOO_ROW1
+#define BM_LOO_ROW1 0  // LOO: a last row tile holding one real row runs as a SIMT pass (A/B)
+#endif
 #ifndef LOO_RR
 #define LOO_RR 1  // 8-row tiles of the nearest set per LOO pass over the candidates
 #endif
@@ -281,6 +290,32 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   int xph = 0;  // exchange-buffer phase (cluster_sum_w0)
 
   // ---------------------------------------------------------------- means
+#if BM_COV1P
+  // one-pass covariance (below) about a shift s: the mean of the first
+  // min(m, 32) candidates (warp 0; every CTA of a cluster gets the same bits).
+  // C = (D - S S^T / m) / (m - 1) with D = sum (z - s)(z - s)^T and S =
+  // sum (z - s) from the same DMMA pass; |mean - s| is a fraction of the
+  // spread, so the correction does not cancel digits.
+  if (warp == 0) {
+    double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
+    const typename ZL::Ref c0 = zv.ref(H, lane), c1 = zv.ref(H, lane < 8 ? 32 + lane : 37);
+    const int ms = min(m, 32);
+    for (int j = 0; j < ms; j += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        if (j + u < ms) {
+          const int b = zv.base(j + u);
+          a0[u] += zv.at(c0, b);
+          a1[u] += zv.at(c1, b);
+        }
+      }
+    }
+    H.mean[lane] = ((a0[0] + a0[1]) + (a0[2] + a0[3])) / ms;
+    if (lane < 8) H.mean[32 + lane] = ((a1[0] + a1[1]) + (a1[2] + a1[3])) / ms;
+  }
+  __syncthreads();
+  BM_PHASE(1);
+#else
   {
     // 4 independent accumulator pairs per lane (loads overlap), fixed-order combine
     double a0[4] = {0.0, 0.0, 0.0, 0.0}, a1[4] = {0.0, 0.0, 0.0, 0.0};
@@ -333,6 +368,8 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     BM_PHASE(1);
   }
 
+#endif
+
   // ------------------------------------------------- covariance (DMMA)
   {
     typename ZL::Ref cr[5];
@@ -343,9 +380,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       cr[tl] = zv.ref(H, col);
       mu[tl] = H.mean[col];
     }
-    double acc[28];
+    constexpr int NCACC = BM_COV1P ? 30 : 28;  // (+ the (x|1, x|1) tile: the sums S of the x columns)
+    double acc[NCACC];
 #pragma unroll
-    for (int i = 0; i < 28; i++) acc[i] = 0.0;
+    for (int i = 0; i < NCACC; i++) acc[i] = 0.0;
     // software pipeline: the next k-step's fragments load during this step's MMAs
     with_na(n, [&](auto NAc) {
     constexpr int NA = decltype(NAc)::value;
@@ -363,6 +401,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         const double raw = zv.at(cr[tl], b);
         o[tl] = valid ? raw - mu[tl] : 0.0;
       }
+      if (BM_COV1P && g == ONES_COL - 32) o[4] = valid ? 1.0 : 0.0;  // column of ones: S = sum (z - s)
     };
     load_f(gw, f);
 #pragma unroll kCovUnroll
@@ -376,17 +415,32 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           if (a < NA && (bb < NA || bb == 4)) dmma(acc[2 * idx], acc[2 * idx + 1], f[a], f[bb]);
           idx++;
         }
+      if (BM_COV1P) dmma(acc[NCACC - 2], acc[NCACC - 1], f[4], f[4]);
 #pragma unroll
       for (int tl = 0; tl < 5; tl++) f[tl] = fn[tl];
     }
     });
-    tree_reduce<28, 14>(acc, H.R1);
-    cluster_sum_w0<28>(acc, H, xph);
+    tree_reduce<NCACC, NCACC / 2>(acc, H.R1);
+    cluster_sum_w0<NCACC>(acc, H, xph);
     double* cyy = H.R1 + R1_SIZE - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
     double* L = cyy + 32 * 33;
     __syncwarp();
     if (warp == 0) {
       const double inv = 1.0 / (double)(m - 1);
+#if BM_COV1P
+      // S from the ones column (C column 36: lanes t4 == 2, element 0)
+      double* Ssum = H.wmin[0];
+      if (t4 == 2) {
+        int id = 0;
+#pragma unroll
+        for (int a = 0; a < 4; a++) {
+          id += 5 - a;  // tiles (a, a..4): idx of tile (a, 4) = id - 1
+          Ssum[8 * a + g] = acc[2 * (id - 1)];
+        }
+        Ssum[32 + g] = acc[NCACC - 2];
+      }
+      __syncwarp();
+#endif
       int idx = 0;
 #pragma unroll
       for (int a = 0; a < 4; a++)
@@ -395,7 +449,11 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
           for (int e = 0; e < 2; e++) {
             const int ra = 8 * a + g, cb = 8 * bb + 2 * t4 + e;
+#if BM_COV1P
+            const double v = fma(-Ssum[ra], Ssum[cb] / m, acc[2 * idx + e]) / (double)(m - 1);
+#else
             const double v = acc[2 * idx + e] / (double)(m - 1);
+#endif
             if (bb < 4) {
               if (ra < n && cb < n && ra <= cb) {
                 cyy[ra * 33 + cb] = v;
@@ -762,7 +820,11 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     for (int s = gw; s < nks; s += GWARPS) {
       load_b(s + GWARPS, dln, fbn);
       double fa[3];
+#if BM_LOO_FAST
+      const double e2w = brow ? exp_wf(dl * sc2, exptab) : 0.0;  // exp(expo - expo.max()); -inf -> 0
+#else
       const double e2w = brow ? exp_wn(dl * sc2, exptab) : 0.0;  // exp(expo - expo.max()); -inf -> 0
+#endif
       fa[2] = e2w;
       fa[1] = e2w * e2w;
       fa[0] = fa[1] * fa[1];
@@ -891,7 +953,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   // tiles per pass bound registers; the Gram B fragments (y0 - y_j) are
   // re-read from the shared support tile each pass.
   double* Zp = H.R1 + ZP_OFF;  // [KMAX][40], after the <=20-tile tree-reduction partials
-  const int ntile = (k + 7) >> 3;  // 8-row tiles of the nearest set
+  // 8-row tiles of the nearest set on DMMA; with k = 8t + 1 (N_y = 16 / 24 /
+  // 32), the last row runs as a SIMT pass below instead of a 1-of-8-rows tile
+  const bool row1 = BM_LOO_ROW1 && CS == 1 && (k & 7) == 1 && k > 8;
+  const int ntile = (k + 7 - (row1 ? 1 : 0)) >> 3;
   constexpr int RR = LOO_RR;       // row tiles per pass over the candidates
   double y0r[8];
   typename ZL::Ref ry[8];
@@ -944,6 +1009,31 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         }
         g0 += h0;
         g1 += h1;
+#if BM_LOO_FAST
+        // -q_ij = 2 G_ij - (d_i + d_j); x = -q sb (sb a power of two) and
+        // x - xref in one fma; the row-max vote compares bit patterns on the
+        // integer pipe (a > 20 <=> bits(a) > bits(20) for non-NaN a)
+        const bool v0 = nri >= 0 && col < m && col != nri, v1 = nri >= 0 && col + 1 < m && col + 1 != nri;
+        const double u0 = fma(2.0, g0, -(dni + dv0)), u1 = fma(2.0, g1, -(dni + dv1));
+        double a0 = fma(u0, sb, -xref[rr]), a1 = fma(u1, sb, -xref[rr]);
+        constexpr long long B20 = 0x4034000000000000ll;  // bits of 20.0
+        if (__any_sync(FULL, (v0 && __double_as_longlong(a0) > B20) || (v1 && __double_as_longlong(a1) > B20))) {
+          // (rare) raise the row references, rescale the rows' partial sums
+          double tmax = fmax(v0 ? u0 * sb : -INFINITY, v1 ? u1 * sb : -INFINITY);
+          tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 1));
+          tmax = fmax(tmax, __shfl_xor_sync(FULL, tmax, 2));
+          if (tmax > xref[rr] + 20.0) {
+            const double f = xref[rr] == -INFINITY ? 0.0 : exp(xref[rr] - tmax);
+#pragma unroll
+            for (int q = 0; q < 10; q++) acc[rr * 10 + q] *= f;
+            xref[rr] = tmax;
+            a0 = fma(u0, sb, -tmax);
+            a1 = fma(u1, sb, -tmax);
+          }
+        }
+        const double e0 = exp_wf(a0, exptab), e1 = exp_wf(a1, exptab);
+        const double w0 = v0 ? e0 : 0.0, w1 = v1 ? e1 : 0.0;  // (invalid: a may be +inf, e garbage)
+#else
         double x0 = -INFINITY, x1 = -INFINITY;
         if (nri >= 0) {
           if (col < m && col != nri) x0 = -(dni + dv0 - 2.0 * g0) * sb;
@@ -962,14 +1052,15 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           }
         }
         const double e0 = exp_wn(x0 - xref[rr], exptab), e1 = exp_wn(x1 - xref[rr], exptab);
-        const double a0 = x0 == -INFINITY ? 0.0 : e0, a1 = x1 == -INFINITY ? 0.0 : e1;  // (xref may be -inf)
+        const double w0 = x0 == -INFINITY ? 0.0 : e0, w1 = x1 == -INFINITY ? 0.0 : e1;  // (xref may be -inf)
+#endif
 #pragma unroll
         for (int ct = 0; ct < 5; ct++) {
           if (ct >= NA && ct < 4) continue;  // y columns beyond n: outputs unused
           const double z0 = ct == 4 && ones ? 1.0 : zv.at(crz[ct], b0);  // padding: weight 0
           const double z1 = ct == 4 && ones ? 1.0 : zv.at(crz[ct], b1);
-          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a0, z0);
-          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], a1, z1);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], w0, z0);
+          dmma(acc[rr * 10 + 2 * ct], acc[rr * 10 + 2 * ct + 1], w1, z1);
         }
       }
     }
@@ -1040,6 +1131,78 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
     }
   }
+#if BM_LOO_ROW1
+  if (row1) {
+    // Row i = k - 1 of the LOO sums: lanes are candidates for the Gram entry
+    // G_ij = U_i . (y0 - y_j) and the weight, then lanes are columns (y, x,
+    // ones) for Zp_i = sum_j w_ij [Y|X|1]_j; a lazily raised per-warp
+    // reference as in the DMMA passes, warps combined at the common maximum
+    // in a fixed order.
+    const int i = k - 1;
+    const int nri = H.near[i];
+    const double dni = H.dn[i];
+    const int ncol = n + 5;
+    auto colof = [&](int c) { return c < n ? c : (c < n + 4 ? 32 + c - n : ONES_COL); };
+    const int cA = colof(lane), cB = colof(min(lane + 32, ncol - 1));
+    const typename ZL::Ref rA = zv.ref(H, cA < 36 ? cA : 0), rB = zv.ref(H, cB < 36 ? cB : 0);
+    const bool hasA = lane < ncol, hasB = lane + 32 < ncol;
+    const double* Ui = Un + i * LS;
+    double sA0 = 0.0, sA1 = 0.0, sB = 0.0, xr = -INFINITY;
+    for (int j0 = warp * 32; j0 < m; j0 += NT) {
+      const int j = j0 + lane;
+      const bool v = j < m && j != nri;
+      const int jc = min(j, m - 1);
+      const int b = zv.base(jc);
+      double ga = 0.0, gb = 0.0;
+#pragma unroll 4
+      for (int t = 0; t < n; t += 2) {
+        ga = fma(Ui[t], y0[t] - zv.at(zv.ref(H, t), b), ga);
+        if (t + 1 < n) gb = fma(Ui[t + 1], y0[t + 1] - zv.at(zv.ref(H, t + 1), b), gb);
+      }
+      const double x = -(dni + dS[jc] - 2.0 * (ga + gb)) * sb;
+      const double wx = warp_max(v ? x : -INFINITY);
+      if (wx > xr + 20.0) {  // (rare) raise the warp's reference, rescale its sums
+        const double f = xr == -INFINITY ? 0.0 : exp(xr - wx);
+        sA0 *= f;
+        sA1 *= f;
+        sB *= f;
+        xr = wx;
+      }
+      const double w = v ? exp_wn(x - xr, exptab) : 0.0;
+      const int cnt = min(32, m - j0);
+#pragma unroll 2
+      for (int jj = 0; jj < cnt; jj++) {
+        const double wj = __shfl_sync(FULL, w, jj);
+        const int bj = __shfl_sync(FULL, b, jj);
+        const double za = cA == ONES_COL ? 1.0 : zv.at(rA, bj);
+        if (jj & 1) sA1 = fma(wj, za, sA1);
+        else sA0 = fma(wj, za, sA0);
+        if (hasB) sB = fma(wj, cB == ONES_COL ? 1.0 : zv.at(rB, bj), sB);
+      }
+    }
+    double* ws = H.R1;  // [NWARP][40] (free: the tree-reduction partials of the passes above)
+    if (hasA) ws[warp * 40 + cA] = sA0 + sA1;
+    if (hasB) ws[warp * 40 + cB] = sB;
+    if (lane == 0) H.redmin[0][warp] = xr;
+    __syncthreads();
+    if (warp == 0) {
+      double M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) M = fmax(M, H.redmin[0][w]);
+      double fw[NWARP];
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) fw[w] = H.redmin[0][w] == -INFINITY ? 0.0 : exp(H.redmin[0][w] - M);
+      double tA = 0.0, tB = 0.0;
+#pragma unroll
+      for (int w = 0; w < NWARP; w++) {
+        if (hasA) tA = fma(ws[w * 40 + cA], fw[w], tA);
+        if (hasB) tB = fma(ws[w * 40 + cB], fw[w], tB);
+      }
+      if (hasA) Zp[i * 40 + cA] = tA;
+      if (hasB) Zp[i * 40 + cB] = tB;
+    }
+  }
+#endif
   __syncthreads();
   BM_PHASE(11);
 

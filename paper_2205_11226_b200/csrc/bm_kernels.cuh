@@ -1145,6 +1145,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
     if (P.build) want = P.build;
     const int mine = NT <= 256 ? 256 : (CS > 1 ? BUILD_CLUSTER : 512);
     if (mine != want) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.counters[6] = (unsigned long long)mine;  // the build that ran
   }
   const unsigned crank = cluster_rank();
   const long long t_cta0 = clock64();
@@ -1324,6 +1325,7 @@ __global__ void k_summary(KParams P, bm_summary* out) {
     s.flop32 = (int64_t)P.counters[9];
     s.hql_patches = (int64_t)P.counters[10];
     s.gate_candidates = (int64_t)P.counters[11];
+    s.kernel_build = (int32_t)P.counters[6];
     *out = s;
   }
 }

@@ -244,6 +244,7 @@ def conceal_batch(
                 "flop32": int(s.flop32),
                 "hql_patches": int(s.hql_patches),
                 "gate_candidates": int(s.gate_candidates),
+                "kernel_build": {256: "256", 512: "512", 1024: "cluster"}.get(int(s.kernel_build)),
             }
             if s.bad_states:
                 _native.check(_native.BM_ERR_STATES)

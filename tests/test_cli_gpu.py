@@ -10,6 +10,8 @@ import numpy as np
 import pytest
 
 from paper_2205_11226_b200 import cli
+from paper_2205_11226_b200.image import BlockGrid
+from paper_2205_11226_b200.loss import gen_dispersed_mask, gen_random_mask
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "aux", "cli")
@@ -19,6 +21,31 @@ RUNS = {
     "dispersed_lost": ["--pattern", "dispersed", "--method", "skmmse", "--t-phi", "12", "--t-nu", "0.05",
                        "--psnr-lost-only"],
 }
+
+
+def _tie_cells(d, lost):
+    """Cells whose pixels differ by > 1 LSB (in raster order, not already
+    excluded: the roots) and their later-raster lost 8-neighbour descendants
+    (tests/parity.py); returns (roots, mask of the pixels still checked)."""
+    H, W = lost.shape
+    gr, gc = H // 16, W // 16
+    cl = lost[: gr * 16, : gc * 16].reshape(gr, 16, gc, 16).any(axis=(1, 3))
+    big = (d > 1)[: gr * 16, : gc * 16].reshape(gr, 16, gc, 16).any(axis=(1, 3))
+    excl = np.zeros((gr, gc), bool)
+    roots = []
+    for r in range(gr):
+        for c in range(gc):
+            if not cl[r, c]:
+                continue
+            if any(0 <= r + dr < gr and 0 <= c + dc < gc and excl[r + dr, c + dc]
+                   for dr, dc in ((-1, -1), (-1, 0), (-1, 1), (0, -1))):
+                excl[r, c] = True
+            elif big[r, c]:
+                excl[r, c] = True
+                roots.append((r, c))
+    keep = lost.copy()
+    keep[: gr * 16, : gc * 16] &= ~np.repeat(np.repeat(excl, 16, axis=0), 16, axis=1)
+    return roots, keep
 
 
 def _pgm(buf):
@@ -44,19 +71,30 @@ def test_cli_matches_reference_run(native, tmp_path, run):
         assert abs(a["psnr_db"] - b["psnr_db"]) <= 0.05, (a["psnr_db"], b["psnr_db"])  # +-1 LSB on <=0.1% px
         assert abs(a["ssim"] - b["ssim"]) <= 1e-3
     files = np.load(os.path.join(GOLD, f"{run}_files.npz"))
+    masks = {}
+    for a in ours["images"]:
+        nm = os.path.splitext(os.path.basename(a["image"]))[0]
+        img = _pgm(open(os.path.join(GOLD, nm + ".pgm"), "rb").read())
+        grid = BlockGrid(img.shape[1], img.shape[0])
+        m = gen_random_mask(grid, 0.3, 5) if run == "random" else gen_dispersed_mask(grid)
+        masks[nm] = np.asarray(m.states)
     for name in files.files:
         got = np.fromfile(tmp_path / name, dtype=np.uint8)
         exp = files[name]
         assert got.shape == exp.shape, name
         if name.endswith(".recon.pgm"):
-            # the +-1 LSB bar, except where a beta choice the reference itself made
-            # at rounding level moved a few cells (decision-level parity, with the
-            # tie rule, is tests/test_gpu.py's): those stay few and local
+            # the tests/parity.py rule on the output files: a beta choice the
+            # reference itself made at rounding level may move a cell (decision-
+            # level parity with the tie rule is tests/test_gpu.py's); that cell
+            # and its later-raster lost 8-neighbour descendants leave the bar,
+            # the first divergences are counted, every other lost pixel is
+            # within +-1 with at most 0.1% off
             g, e = _pgm(got).astype(int), _pgm(exp).astype(int)
-            d = np.abs(g - e)
-            big = d > 1
-            cells = {(r // 16, c // 16) for r, c in zip(*np.nonzero(big))}
-            assert (d > 0).mean() <= 0.01 and len(cells) <= 3, (name, int(d.max()), sorted(cells))
+            lost = masks[name.split(".")[0]] == 1
+            roots, keep = _tie_cells(np.abs(g - e), lost)
+            d = np.abs(g - e)[keep]
+            assert len(roots) <= 1, (name, roots)
+            assert d.max(initial=0) <= 1 and (d > 0).sum() <= max(1, 0.001 * lost.sum()), (name, int(d.max()))
         else:
             assert np.array_equal(got, exp), name
     # CSV schema
