@@ -103,3 +103,21 @@ def test_cli_matches_reference_run(native, tmp_path, run):
     assert rc == 0
     head = open(tmp_path / "csv" / "report.csv").readline().strip().split(",")
     assert head == cli.CSV_COLUMNS
+
+
+def test_cli_parallel_equals_serial(native, tmp_path):
+    """--parallel (host staging on a thread pool) gives the serial run's
+    report rows and output files (the reference's test_cli.py:178-189)."""
+    args = ["--input", os.path.join(GOLD, "img_*.pgm"), *RUNS["random"]]
+    assert cli.main([*args, "--out-dir", str(tmp_path / "s")]) == 0
+    assert cli.main([*args, "--out-dir", str(tmp_path / "p"), "--parallel"]) == 0
+    rs = json.load(open(tmp_path / "s" / "report.json"))
+    rp = json.load(open(tmp_path / "p" / "report.json"))
+    timing = {"total_s", "mean_patch_ms", "wall_s", "elapsed_s"}
+    strip = lambda rows: [{k: v for k, v in r.items() if k not in timing} for r in rows]
+    assert strip(rs["images"]) == strip(rp["images"])
+    names = sorted(os.listdir(tmp_path / "s"))
+    assert names == sorted(os.listdir(tmp_path / "p"))
+    for nm in names:
+        if nm.endswith((".pgm", ".ppm")):
+            assert (tmp_path / "s" / nm).read_bytes() == (tmp_path / "p" / nm).read_bytes(), nm
