@@ -135,27 +135,41 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32], int lan
   return v[0];
 }
 
-// NumPy's pairwise summation order for n <= 128 elements (the order of
-// ndarray.sum along a contiguous axis), so BRL means and Euclidean distances
-// are bit-identical to the reference for any inputs.
+// NumPy's pairwise summation order (numpy/_core/src/umath/loops_utils.h.src
+// pairwise_sum: the order of ndarray.sum along a contiguous axis), so BRL
+// means, Euclidean distances and the alpha sums are bit-identical to the
+// reference for any inputs.  Blocks of <= 128 elements use eight strided
+// accumulators; longer runs split at n/2 rounded down to a multiple of 8
+// (pairwise_sum_long: one level, n <= 256).
 template <typename F>
-__device__ __forceinline__ double pairwise_sum_n(int n, F a) {
+__device__ __forceinline__ double pairwise_block(int lo, int n, F a) {
   if (n < 8) {
     double res = 0.0;
-    for (int i = 0; i < n; i++) res += a(i);
+    for (int i = 0; i < n; i++) res += a(lo + i);
     return res;
   }
   double r[8];
 #pragma unroll
-  for (int j = 0; j < 8; j++) r[j] = a(j);
+  for (int j = 0; j < 8; j++) r[j] = a(lo + j);
   int i = 8;
   for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-    for (int j = 0; j < 8; j++) r[j] += a(i + j);
+    for (int j = 0; j < 8; j++) r[j] += a(lo + i + j);
   }
   double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-  for (; i < n; i++) res += a(i);
+  for (; i < n; i++) res += a(lo + i);
   return res;
+}
+template <typename F>
+__device__ __forceinline__ double pairwise_sum_n(int n, F a) {  // n <= 128
+  return pairwise_block(0, n, a);
+}
+template <typename F>
+__device__ __forceinline__ double pairwise_sum_long(int n, F a) {  // n <= 256
+  if (n <= 128) return pairwise_block(0, n, a);
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pairwise_block(0, n2, a) + pairwise_block(n2, n - n2, a);
 }
 
 // Chebyshev ring geometry of one patch's expansion map (framework.py:130-148),

@@ -71,6 +71,12 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_LOO_ROW1
 #define BM_LOO_ROW1 0  // LOO: a last row tile holding one real row runs as a SIMT pass (A/B)
 #endif
+#ifndef BM_NEAR2
+#define BM_NEAR2 1  // nearest-set distances two candidates per pass (bit-identical) (A/B)
+#endif
+#ifndef BM_LINV_N
+#define BM_LINV_N 1  // L^-1 substitution stops at row n (bit-identical) (A/B)
+#endif
 #ifndef LOO_RR
 #define LOO_RR 1  // 8-row tiles of the nearest set per LOO pass over the candidates
 #endif
@@ -532,21 +538,28 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
       // L^-1 in registers: lane c builds column c by forward substitution
       // (L rows read as shared-memory broadcasts); identity beyond n
+      // (rows i >= n are identity rows: they never feed rows < n and are
+      // stored as zeros, so the substitution stops at n)
       double x[32];
 #pragma unroll
       for (int i = 0; i < 32; i++) {
-        double s0 = 0.0, s1 = 0.0;
+        x[i] = 0.0;
+        if (!BM_LINV_N || i < n) {  // warp-uniform
+          double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < i; k++) {
-          const double lik = L[i * 33 + k];
-          if (k & 1) s1 = fma(lik, x[k], s1);
-          else s0 = fma(lik, x[k], s0);
+          for (int k = 0; k < i; k++) {
+            const double lik = L[i * 33 + k];
+            if (k & 1) s1 = fma(lik, x[k], s1);
+            else s0 = fma(lik, x[k], s0);
+          }
+          const double rdi = H.rdiag[i];
+          x[i] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);
         }
-        const double rdi = H.rdiag[i];
-        x[i] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);
       }
+      if (lane == 0) BM_DIAG_ADD(38, (clock64() - ph_t));  // + L^-1 (diagnostic)
 #pragma unroll
       for (int i = 0; i < 32; i++) H.Linv[i * LS + lane] = (i < n && lane < n) ? x[i] : 0.0;  // zero beyond n
+      if (lane == 0) BM_DIAG_ADD(39, (clock64() - ph_t));  // + Linv stored (diagnostic)
     } else {
       // warps 1..7: Euclidean distances in NumPy's order and the stable
       // k-nearest selection (optimize_alpha, estimators.py:221-223)
@@ -560,6 +573,47 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // (n < 8: tail only).  One candidate per thread, read from the tile.
       // Column refs and y0 are shared-memory broadcasts.
       const int n8 = n - (n % 8);
+#if BM_CNEAR && BM_NEAR2
+      // two candidates per pass: the column offsets and y0 are loaded once
+      // for both; each candidate keeps NumPy's order (the same operations as
+      // the one-candidate form below, so the same bits)
+#pragma unroll 1
+      for (int i = 0; i < PER; i += 2) {
+        const int ja = (t7 + i * NW7) * CS + (int)rank;
+        const int jb = (t7 + (i + 1) * NW7) * CS + (int)rank;
+        if (ja < m) {
+          const bool hb = i + 1 < PER && jb < m;
+          const int ba = zv.base(ja), bb = zv.base(hb ? jb : ja);
+          double ra[8], rb[8];
+#pragma unroll
+          for (int q = 0; q < 8; q++) ra[q] = rb[q] = 0.0;
+#pragma unroll 1
+          for (int q0 = 0; q0 < n8; q0 += 8)
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+              const typename ZL::Ref rq = zv.ref(H, q0 + q);
+              const double yq = y0[q0 + q];
+              const double da = __dsub_rn(zv.at(rq, ba), yq), db = __dsub_rn(zv.at(rq, bb), yq);
+              ra[q] = __dadd_rn(ra[q], __dmul_rn(da, da));
+              rb[q] = __dadd_rn(rb[q], __dmul_rn(db, db));
+            }
+          double ea = __dadd_rn(__dadd_rn(__dadd_rn(ra[0], ra[1]), __dadd_rn(ra[2], ra[3])),
+                                __dadd_rn(__dadd_rn(ra[4], ra[5]), __dadd_rn(ra[6], ra[7])));
+          double eb = __dadd_rn(__dadd_rn(__dadd_rn(rb[0], rb[1]), __dadd_rn(rb[2], rb[3])),
+                                __dadd_rn(__dadd_rn(rb[4], rb[5]), __dadd_rn(rb[6], rb[7])));
+#pragma unroll 1
+          for (int q = n8; q < n; q++) {
+            const typename ZL::Ref rq = zv.ref(H, q);
+            const double yq = y0[q];
+            const double da = __dsub_rn(zv.at(rq, ba), yq), db = __dsub_rn(zv.at(rq, bb), yq);
+            ea = __dadd_rn(ea, __dmul_rn(da, da));
+            eb = __dadd_rn(eb, __dmul_rn(db, db));
+          }
+          dS[ja] = ea;
+          if (hb) dS[jb] = eb;
+        }
+      }
+#else
 #if BM_CNEAR
       // rolled over the thread's candidates (compact code); each thread
       // stages its own distances in dS (free until the quadforms)
@@ -596,6 +650,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #endif
         }
       }
+#endif  // BM_CNEAR && BM_NEAR2
 #if BM_CNEAR
 #pragma unroll
       for (int i = 0; i < PER; i++) {
@@ -1242,10 +1297,16 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       double corr[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) corr[q] = warp_sum(H.Bm[q * 32 + lane] * u0);
+      // den = (c * c).sum() on lane 0, num = ((x - x_pred).T * c).sum() on
+      // lane 1 (NumPy's pairwise order over the 4k elements), concurrently
+      const int kk = 4 * k;
+      double sv = 0.0;
+      if (lane < 2) {
+        const double* f = lane ? H.rmat : H.cmat;
+        sv = pairwise_sum_long(kk, [&](int i) { return __dmul_rn(f[i], H.cmat[i]); });
+      }
+      const double den = __shfl_sync(FULL, sv, 0), num = __shfl_sync(FULL, sv, 1);
       if (lane == 0) {
-        const int kk = 4 * k;
-        const double den = pairwise_sum_n(kk, [&](int i) { return __dmul_rn(H.cmat[i], H.cmat[i]); });
-        const double num = pairwise_sum_n(kk, [&](int i) { return __dmul_rn(H.rmat[i], H.cmat[i]); });
         double a = 0.0;
         if (!(den < 1e-12)) {
           a = num / den;
