@@ -80,8 +80,10 @@ typedef struct bm_patch_record {
   uint8_t rings_used;   /* LayerDecision.rings_used */
   int32_t m_candidates; /* valid if BM_REC_HAS_M */
   uint32_t cycles;      /* SM clock cycles spent on the patch (-> elapsed_s) */
-  float beta_gap;       /* HQL: min over other grid betas of (eps_g - eps_best)/eps_best;
-                           a near-tie (< ~1e-12) is rounding-decided (parity harness) */
+  float beta_gap;       /* HQL: min over the other grid betas of |eps_g - eps_best|, in units of
+                           the eps change a 1e-11 relative perturbation of y0 can cause
+                           (2 sqrt(eps_best N_y) dy + N_y dy^2, dy = 1e-11 max|y0|); < 1 means
+                           the choice was decided at rounding level (tests/parity.py) */
   uint32_t pad;
   double phi, nu, beta, alpha;
 } bm_patch_record;
@@ -130,8 +132,9 @@ int64_t bm_max_records(const bm_params* p);
  * launch; up to 256 kept).  Synchronises on the events.  Returns the count. */
 int bm_kernel_times_ms(float* out, int cap);
 void bm_kernel_times_reset(void);
-/* Diagnostics: 40 cumulative SM-cycle counters (HQL phases, IDL patch
- * phases, scheduling); names in _native.PHASES. */
+/* Diagnostics: 48 cumulative SM-cycle counters (HQL phases, IDL patch
+ * phases, scheduling; filled only by -DBM_DIAG=1 builds); names in
+ * _native.PHASES. */
 int bm_debug_phase_cycles(unsigned long long* out48, int reset);
 /* ---- callers either side of the path ---------- */
 

@@ -29,6 +29,8 @@ int orc_conceal_dag(int H, int W, const double* pixels, const uint8_t* states, d
                     double sigma2, int forced_layer, double* out_pixels, orc_record* out_records,
                     long max_records, long* out_nrec, long* out_lost_cells, int threads);
 void orc_brl(const double* y0, int n, double* out4);
+/* NumPy's pairwise summation of a[0..n) (test hook for tests/test_oracle_numerics.py) */
+double orc_pairwise_sum(const double* a, long n);
 int orc_idl(const double* y0, int n, const double* x, const double* y, int m, double sigma2,
             double* out4, double* raw_sum);
 int orc_hql(const double* y0, int n, const double* x, const double* y, int m, double sigma2,

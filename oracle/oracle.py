@@ -84,6 +84,8 @@ def lib():
                                  ctypes.POINTER(_Info)]
         _lib.orc_idl.argtypes = [dp, ctypes.c_int, dp, dp, ctypes.c_int, ctypes.c_double, dp, dp]
         _lib.orc_brl.argtypes = [dp, ctypes.c_int, dp]
+        _lib.orc_pairwise_sum.restype = ctypes.c_double
+        _lib.orc_pairwise_sum.argtypes = [dp, ctypes.c_long]
     return _lib
 
 
@@ -156,6 +158,12 @@ def idl(y0, x, y, sigma2=10.0):
     raw = ctypes.c_double(0.0)
     rc = lib().orc_idl(_dp(y0p), n, _dp(xx), _dp(yy), m, sigma2, _dp(out), ctypes.byref(raw))
     return (None if rc else out), raw.value
+
+
+def pairwise_sum(a):
+    """The oracle's restatement of NumPy's pairwise summation (test hook)."""
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return lib().orc_pairwise_sum(_dp(a), a.size)
 
 
 def brl(y0):
