@@ -728,19 +728,43 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
       cluster_sync_all();
       if (warp == 0) {
-        const uint32_t base = map_rank(b, lane < CS ? lane : 0);
-        int ptr = 0;
-        for (int it = 0; it < k; it++) {
-          double hv = INFINITY;
-          int hj = 0x7fffffff;
-          if (lane < CS && ptr < k) {
-            hv = ld_dsmem_f64(base + ptr * 8u);
-            hj = (int)ld_dsmem_f64(base + (KMAX + ptr) * 8u);
+        // copy the CS sorted lists in one DSMEM round trip, then rank every
+        // entry: its position in its own list + the entries of the other
+        // lists that precede it in the (distance, index) order (a total
+        // order: the lists hold disjoint candidates); the first k ranks are
+        // the cluster's k nearest, the same set and order as a head-by-head
+        // merge
+        double* cv = H.R2;                                       // [CS][KMAX]
+        int* cj = reinterpret_cast<int*>(H.R2 + CS * KMAX);       // [CS][KMAX]
+#pragma unroll
+        for (int r = 0; r < CS; r++) {
+          const uint32_t base = map_rank(b, r);
+          for (int e = lane; e < k; e += 32) {
+            cv[r * KMAX + e] = ld_dsmem_f64(base + e * 8u);
+            cj[r * KMAX + e] = (int)ld_dsmem_f64(base + (KMAX + e) * 8u);
           }
-          int bj;
-          warp_argmin_key(hv, hj, bj);
-          if (lane == 0) H.near[it] = bj;
-          if (lane < CS && hj == bj) ptr++;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < CS; r++) {
+          for (int e = lane; e < k; e += 32) {
+            const double v = cv[r * KMAX + e];
+            const int j = cj[r * KMAX + e];
+            int rank = e;
+#pragma unroll
+            for (int o = 0; o < CS; o++) {
+              if (o == r) continue;
+              int lo = 0, hi = k;  // entries of list o before (v, j)
+              while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                const double mv = cv[o * KMAX + mid];
+                if (mv < v || (mv == v && cj[o * KMAX + mid] < j)) lo = mid + 1;
+                else hi = mid;
+              }
+              rank += lo;
+            }
+            if (rank < k) H.near[rank] = j;
+          }
         }
       }
       xph ^= 1;

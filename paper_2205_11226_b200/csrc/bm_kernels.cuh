@@ -82,6 +82,7 @@ struct CellSmem {
   unsigned long long remaining, pend;
   int deferred[64];
   int ndef, progressed, nrec;
+  int readers;  // some later-raster lost 8-neighbour will read cellbuf
   int pick, skip, gated_stop;
   int m, rings_used, max_ring, K, cur_ring;
   double nu, carry, phi;
@@ -1188,9 +1189,15 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
         bits |= (unsigned long long)b << (32 * h);
         S.pkey[p] = patch_key(S, p);
       }
+      // later-raster lost 8-neighbours read this cell's values from cellbuf;
+      // with none, the FP64 publish is skipped (DRAM writes)
+      int ps;
+      const int dr = tid == 0 ? 0 : 1, dc = tid == 0 ? 1 : tid - 2;
+      const unsigned rd = __ballot_sync(FULL, tid < 4 && cell_lost(P, S.f, S.gr + dr, S.gc + dc, ps));
       if (tid == 0) {
         S.remaining = bits;
         S.nrec = 0;
+        S.readers = rd != 0u;
       }
     }
     __syncthreads();
@@ -1267,7 +1274,7 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
       for (int i = tid; i < 256; i += NT) {
         const int rr = i / BS, cc = i % BS;
         const double v = S.tile[(BS + rr) * TS + BS + cc];
-        P.cellbuf[slot * 256 + i] = v;
+        if (S.readers) P.cellbuf[slot * 256 + i] = v;
         const size_t o = ((size_t)f * P.H + r0 + rr) * P.W + c0 + cc;
         if (P.out_f64) P.out_f64[o] = v;
         if (P.out_u8) P.out_u8[o] = (uint8_t)floor(fmin(fmax(v, 0.0), 255.0) + 0.5);  // image.py:53-56
