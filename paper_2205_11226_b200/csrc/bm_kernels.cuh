@@ -1176,7 +1176,17 @@ __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1) k_conceal(KParams P) {
     }
     __syncthreads();
     if (tid == 0) BM_DIAG_ADD(20, (clock64() - t_w0));  // scheduling wait
+    const long long t_lt = clock64();
     load_tile(P, S);
+    if (tid == 0) {  // the staging (gather) stage: cycles, cells, finished-neighbour buffers read (diagnostic)
+      BM_DIAG_ADD(40, (clock64() - t_lt));
+      BM_DIAG_ADD(41, 1);
+#if BM_DIAG
+      int nb = 0, ps;
+      for (int q = 0; q < 4; q++) nb += cell_lost(P, S.f, S.gr - 1 + (q < 3 ? 0 : 1), S.gc - 1 + (q < 3 ? q : 0), ps);
+      BM_DIAG_ADD(42, nb);
+#endif
+    }
     // lost_patch_origins (framework.py:219-227)
     if (tid < 32) {
       unsigned long long bits = 0;

@@ -46,3 +46,9 @@ print(f"loo: loops(t0) {ph['loo_loops_t0'] / max(n_hql,1):.0f}  (phase total {ph
 print("nearest (from HQL start): e2 %.0f sorted %.0f warp-merged %.0f all-merged %.0f final %.0f" % tuple(
     ph[k] / max(n_hql, 1) for k in ("e2_done", "nn_sorted", "nn_warp_merged", "nn_all_merged", "nearest")))
 print(f"per-patch cycles: IDL {ph['patch_idl'] / max(nidl, 1):.0f}  HQL {ph['patch_hql'] / max(n_hql, 1):.0f}  BRL {ph['patch_brl'] / max(r.summary['layer_counts']['BRL'], 1):.0f}")
+lt, nc, nb = ph.get('load_tile', 0), max(ph.get('load_tile_cells', 0), 1), ph.get('load_tile_nbufs', 0)
+if ph.get('load_tile_cells', 0):
+    byt = 2304 * 2 + 2048 * nb / nc  # u8 pixels + states of the 48x48 support, FP64 buffers of finished neighbours
+    cyc = lt / nc
+    print(f"staging (gather stage): {cyc:.0f} cycles/cell, {byt:.0f} B/cell ({nb / nc:.2f} neighbour buffers) "
+          f"-> {byt / (cyc / 1.965e9) / 1e9:.1f} GB/s per CTA; {lt / ph['cta_life'] * 100:.1f}% of CTA time")
