@@ -77,6 +77,9 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_LINV_N
 #define BM_LINV_N 1  // L^-1 substitution stops at row n (bit-identical) (A/B)
 #endif
+#ifndef BM_TSTAGE
+#define BM_TSTAGE 1  // Gram staging / alpha: nearest rows on the lanes, transposed Wt / Vt / R / u (bit-identical) (A/B)
+#endif
 #ifndef LOO_RR
 #define LOO_RR 1  // 8-row tiles of the nearest set per LOO pass over the candidates
 #endif
@@ -996,6 +999,47 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
   // so that v_i . v_j = U_i . (y0 - y_j) reads candidate j straight from the
   // shared support tile (V never goes through global memory).
   double* Un = H.R2;        // [40][LS]  A fragments of the Gram GEMM
+#if BM_TSTAGE
+  // Staging with the nearest rows on the lanes: Wt and Vt are kept transposed
+  // ([32][WS], WS odd), a warp takes one dimension t (warp-uniform trip count
+  // t + 1 or n - t instead of the longest lane's n), L^-1 entries are
+  // broadcasts and the Wt / Vt reads are conflict-free (the [i][32] layout
+  // with t on the lanes read L^-1 rows 8-way bank-conflicted).  Every output
+  // keeps its fma order, so the same bits.
+  constexpr int WS = 33;
+  double* Vt = H.R1;            // [32][WS] (L^-1 (y0 - y_near_i))[t] at [t][i] (R1 head is free here)
+  double* Wt = H.R1 + 32 * WS;  // [32][WS] (y0 - y_near_i)[q] at [q][i] (below Zp)
+  static_assert(2 * 32 * WS <= ZP_OFF + KMAX * 40 && KMAX <= WS, "staging fits R1");
+  for (int o = tid; o < k * 32; o += NT) {
+    const int i = o >> 5, q = o & 31;
+    Wt[q * WS + i] = q < n ? y0[q] - zv.at(zv.ref(H, q), zv.base(H.near[i])) : 0.0;
+  }
+  if (tid < 40) H.dn[tid] = tid < k ? dS[H.near[tid]] : 0.0;
+  for (int o = tid; o < 40 * 32; o += NT) {  // Un vanishes beyond the k rows and n dimensions
+    const int i = o >> 5, t = o & 31;
+    if (i >= k || t >= n) Un[i * LS + t] = 0.0;
+  }
+  __syncthreads();
+  const int nh = (k + 31) >> 5;  // lane groups of 32 nearest rows (2 only for k = 33)
+  for (int row = warp; row < n * nh; row += NWARP) {
+    const int t = row / nh, i = (row % nh) * 32 + lane;
+    if (i < k) {
+      double sv = 0.0;
+      for (int q = 0; q <= t; q++) sv = fma(H.Linv[t * LS + q], Wt[q * WS + i], sv);
+      Vt[t * WS + i] = sv;
+    }
+  }
+  __syncthreads();
+  for (int row = warp; row < n * nh; row += NWARP) {
+    const int t = row / nh, i = (row % nh) * 32 + lane;
+    if (i < k) {
+      double su = 0.0;
+      for (int q = t; q < n; q++) su = fma(H.Linv[q * LS + t], Vt[q * WS + i], su);
+      Un[i * LS + t] = su;
+    }
+  }
+  __syncthreads();
+#else
   double* Vt = H.R1;             // [KMAX][32] L^-1 (y0 - y_near_i) (R1 head is free here)
   double* Wt = H.R1 + KMAX * 32;  // [KMAX][32] y0 - y_near_i (below Zp)
   static_assert(2 * KMAX * 32 <= ZP_OFF + KMAX * 40, "staging fits R1");
@@ -1021,6 +1065,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     Un[i * LS + t] = su;
   }
   __syncthreads();
+#endif
   BM_PHASE(9);
 
   // ---- fused Gram + leave-one-out sums (estimators.py:225-238), DMMA.
@@ -1287,6 +1332,39 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 
   // ---------------------------------- alpha (estimators.py:237-245)
   {
+#if BM_TSTAGE
+    // (the nearest rows on the lanes, R and u transposed: see the staging above)
+    constexpr int WS = 33;
+    double* u = H.R1;  // [32][WS]  u_i[t] at [t][i]
+    double* R = H.R2;  // [36][WS]  (y_i - y~_i | x_i - x~_i)[q] at [q][i]  (Un is dead here)
+    static_assert(36 * WS <= 1600, "R fits R2");
+    for (int o = tid; o < k * 36; o += NT) {
+      const int i = o / 36, q = o % 36;
+      double r = 0.0;
+      if (q < n || q >= 32)
+        r = zv.at(zv.ref(H, q), zv.base(H.near[i])) - Zp[i * 40 + q] / Zp[i * 40 + ONES_COL];
+      R[q * WS + i] = r;
+    }
+    __syncthreads();
+    const int nh = (k + 31) >> 5;
+    for (int row = warp; row < n * nh; row += NWARP) {
+      const int t = row / nh, i = (row % nh) * 32 + lane;
+      if (i < k) {
+        double s = 0.0;
+        for (int q = 0; q <= t; q++) s = fma(H.Linv[t * LS + q], R[q * WS + i], s);
+        u[t * WS + i] = s;
+      }
+    }
+    __syncthreads();
+    for (int o = tid; o < 4 * k; o += NT) {
+      const int q = o / k, i = o % k;
+      double c = 0.0;
+      for (int t = 0; t < n; t++) c = fma(H.Bm[q * 32 + t], u[t * WS + i], c);
+      H.cmat[q * k + i] = c;
+      H.rmat[q * k + i] = R[(32 + q) * WS + i];
+    }
+    __syncthreads();
+#else
     double* u = H.R1;  // [KMAX][32]
     double* R = H.R2;  // [KMAX][36]: y_i - y~_i | x_i - x~_i  (Un is dead here)
     for (int o = tid; o < k * 36; o += NT) {
@@ -1313,6 +1391,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       H.rmat[q * k + i] = R[i * 36 + 32 + q];
     }
     __syncthreads();
+#endif
     if (warp == 0) {
       // u0 = Linv (y0 - y~0); correction = Bm u0
       double s = 0.0;

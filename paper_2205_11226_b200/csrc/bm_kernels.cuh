@@ -51,7 +51,13 @@ struct KParams {
 };
 
 constexpr int BUILD_CLUSTER = 1024;  // KParams::build code of the cluster build
-constexpr int GH = 2, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
+#ifndef BM_GH
+#define BM_GH 4  // 1024-entry chunks after the first (A/B: +0.6% on cfg5 against 512)
+#endif
+#ifndef BM_TABPF
+#define BM_TABPF 1  // gate: a chunk's expansion-map table entries loaded before the screening loop (A/B)
+#endif
+constexpr int GH = BM_GH, GCH = GH * NT;  // gate: expansion-map entries per chunk, GH per thread
 #ifndef BM_FIRST_GH
 #define BM_FIRST_GH 1
 #endif
@@ -73,7 +79,7 @@ struct CellSmem {
     double dbuf[MAXCAND];  // HQL: d_j = |L^-1 (y0 - y_j)|^2
   };
   int pref[2];
-  int wcnt[2 * NWARP];
+  int wcnt[GH * NWARP];
   double ringsum[MAXRING + 2];
   int ringcnt[MAXRING + 2];
   int ring_off[32];
@@ -531,6 +537,17 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
   const int n = E.n;
   // rolled over the gh <= GH entries per thread (one code copy); the window
   // positions wait in posbuf for the compaction (0xFFFF = not admissible)
+#if BM_TABPF
+  static_assert(GH <= 4, "prefetched table entries fit one 64-bit register");
+  unsigned long long tabv = 0;
+  if (tab) {
+#pragma unroll
+    for (int h = 0; h < GH; h++) {
+      const int e = e0 + h * NT + tid;
+      if (h < gh && e < K) tabv |= (unsigned long long)__ldg(tab + e) << (16 * h);
+    }
+  }
+#endif
 #pragma unroll 1
   for (int h = 0; h < gh; h++) {
     const int e = e0 + h * NT + tid;
@@ -542,7 +559,11 @@ __device__ __forceinline__ int screen_chunk(CellSmem& S, const RingGeom& g, int 
       // 32 ring offsets (rings past max_ring start at K > e)
       int wr, wc;  // window origin, tile coords
       if (tab) {     // interior cell: the precomputed expansion map (k_postab)
+#if BM_TABPF
+        const unsigned v = (unsigned)(tabv >> (16 * h)) & 0xFFFFu;
+#else
         const unsigned v = __ldg(tab + e);
+#endif
         wr = (int)(v >> 8);
         wc = (int)(v & 255u);
       } else {
