@@ -77,6 +77,12 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_LINV_N
 #define BM_LINV_N 1  // L^-1 substitution stops at row n (bit-identical) (A/B)
 #endif
+#ifndef BM_LINV_ROLL
+#define BM_LINV_ROLL 1  // L^-1 substitution rolled over the rows, columns kept in shared memory (bit-identical) (A/B)
+#endif
+#ifndef BM_ALPHA_PAR
+#define BM_ALPHA_PAR 1  // alpha den / num pairwise sums on 8-lane groups (bit-identical) (A/B)
+#endif
 #ifndef BM_TSTAGE
 #define BM_TSTAGE 1  // Gram staging / alpha: nearest rows on the lanes, transposed Wt / Vt / R / u (bit-identical) (A/B)
 #endif
@@ -543,6 +549,28 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // (L rows read as shared-memory broadcasts); identity beyond n
       // (rows i >= n are identity rows: they never feed rows < n and are
       // stored as zeros, so the substitution stops at n)
+#if BM_LINV_ROLL
+      // rolled over the rows: column `lane` lives in H.Linv itself (a lane
+      // reads back only its own earlier stores), the even / odd partial sums
+      // as in the unrolled form - the same bits in ~40 instructions instead
+      // of ~1300 straight-line ones per patch (instruction fetch)
+#pragma unroll 1
+      for (int i = 0; i < n; i++) {
+        double s0 = 0.0, s1 = 0.0;
+        int k = 0;
+#pragma unroll 2
+        for (; k + 1 < i; k += 2) {
+          s0 = fma(L[i * 33 + k], H.Linv[k * LS + lane], s0);
+          s1 = fma(L[i * 33 + k + 1], H.Linv[(k + 1) * LS + lane], s1);
+        }
+        if (k < i) s0 = fma(L[i * 33 + k], H.Linv[k * LS + lane], s0);
+        const double rdi = H.rdiag[i];
+        H.Linv[i * LS + lane] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);  // (lanes >= n: zeros)
+      }
+      if (lane == 0) BM_DIAG_ADD(38, (clock64() - ph_t));  // + L^-1 (diagnostic)
+      for (int i = n; i < 32; i++) H.Linv[i * LS + lane] = 0.0;  // zero beyond n
+      if (lane == 0) BM_DIAG_ADD(39, (clock64() - ph_t));  // + Linv stored (diagnostic)
+#else
       double x[32];
 #pragma unroll
       for (int i = 0; i < 32; i++) {
@@ -563,6 +591,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
 #pragma unroll
       for (int i = 0; i < 32; i++) H.Linv[i * LS + lane] = (i < n && lane < n) ? x[i] : 0.0;  // zero beyond n
       if (lane == 0) BM_DIAG_ADD(39, (clock64() - ph_t));  // + Linv stored (diagnostic)
+#endif
     } else {
       // warps 1..7: Euclidean distances in NumPy's order and the stable
       // k-nearest selection (optimize_alpha, estimators.py:221-223)
@@ -1400,6 +1429,33 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       double corr[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) corr[q] = warp_sum(H.Bm[q * 32 + lane] * u0);
+#if BM_ALPHA_PAR
+      // den = (c * c).sum() on lanes 0-15, num = ((x - x_pred).T * c).sum() on
+      // lanes 16-31, in NumPy's pairwise order over the 4k elements (4k >= 8, a
+      // multiple of 4): lane j of an 8-lane group owns the strided accumulator
+      // r[j], the ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) tree is three xor
+      // shuffles, then the tail elements in order; beyond 128 elements the
+      // two halves of NumPy's split run on the two 8-lane groups.  The same
+      // bits as one lane's sequential pairwise_sum_long.
+      const int kk = 4 * k;
+      const int sub = (lane >> 3) & 1, j8 = lane & 7;
+      const double* f = (lane >> 4) ? H.rmat : H.cmat;
+      const bool two = kk > 128;
+      int n2 = kk / 2;
+      n2 -= n2 % 8;
+      const int lo = (two && sub) ? n2 : 0;
+      const int nb = two ? (sub ? kk - n2 : n2) : kk;
+      const int nfull = nb - (nb % 8);
+      double sv = __dmul_rn(f[lo + j8], H.cmat[lo + j8]);
+      for (int i = 8; i < nfull; i += 8) sv = __dadd_rn(sv, __dmul_rn(f[lo + i + j8], H.cmat[lo + i + j8]));
+      sv = __dadd_rn(sv, __shfl_xor_sync(FULL, sv, 1));
+      sv = __dadd_rn(sv, __shfl_xor_sync(FULL, sv, 2));
+      sv = __dadd_rn(sv, __shfl_xor_sync(FULL, sv, 4));
+      for (int i = nfull; i < nb; i++) sv = __dadd_rn(sv, __dmul_rn(f[lo + i], H.cmat[lo + i]));
+      const double sv8 = __shfl_xor_sync(FULL, sv, 8);
+      if (two) sv = __dadd_rn(sv, sv8);
+      const double den = __shfl_sync(FULL, sv, 0), num = __shfl_sync(FULL, sv, 16);
+#else
       // den = (c * c).sum() on lane 0, num = ((x - x_pred).T * c).sum() on
       // lane 1 (NumPy's pairwise order over the 4k elements), concurrently
       const int kk = 4 * k;
@@ -1409,6 +1465,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         sv = pairwise_sum_long(kk, [&](int i) { return __dmul_rn(f[i], H.cmat[i]); });
       }
       const double den = __shfl_sync(FULL, sv, 0), num = __shfl_sync(FULL, sv, 1);
+#endif
       if (lane == 0) {
         double a = 0.0;
         if (!(den < 1e-12)) {
