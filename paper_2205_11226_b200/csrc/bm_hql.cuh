@@ -83,6 +83,12 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_ALPHA_PAR
 #define BM_ALPHA_PAR 1  // alpha den / num pairwise sums on 8-lane groups (bit-identical) (A/B)
 #endif
+#ifndef BM_BETA_PAR
+#define BM_BETA_PAR 1  // beta epilogue: the 21 x n residual divisions on all threads (bit-identical) (A/B)
+#endif
+#ifndef BM_COV_PAR
+#define BM_COV_PAR 1  // covariance epilogue: the divisions by m - 1 on all threads (bit-identical) (A/B)
+#endif
 #ifndef BM_TSTAGE
 #define BM_TSTAGE 1  // Gram staging / alpha: nearest rows on the lanes, transposed Wt / Vt / R / u (bit-identical) (A/B)
 #endif
@@ -439,6 +445,32 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     cluster_sum_w0<NCACC>(acc, H, xph);
     double* cyy = H.R1 + R1_SIZE - 2 * 32 * 33;  // tail of R1 (partials no longer needed)
     double* L = cyy + 32 * 33;
+#if BM_COV_PAR && !BM_COV1P
+    // C = acc / (m - 1): warp 0 stages the 28 reduced tile halves, then all
+    // threads do one division each and scatter into cyy / cxy (one more
+    // barrier instead of 28 divisions per lane on warp 0)
+    if (warp == 0) {
+#pragma unroll
+      for (int i = 0; i < NCACC; i++) H.R2[i * 32 + lane] = acc[i];  // (R2 is free until the nearest-set merge)
+    }
+    __syncthreads();
+    for (int o = tid; o < NCACC * 32; o += NT) {
+      const int vi = o >> 5, ln = o & 31;
+      const int tile = vi >> 1, e = vi & 1;
+      const int a = tile < 5 ? 0 : (tile < 9 ? 1 : (tile < 12 ? 2 : 3));
+      const int bb = tile - (a == 0 ? 0 : (a == 1 ? 5 : (a == 2 ? 9 : 12))) + a;
+      const int ra = 8 * a + (ln >> 2), cb = 8 * bb + 2 * (ln & 3) + e;
+      const double v = H.R2[o] / (double)(m - 1);
+      if (bb < 4) {
+        if (ra < n && cb < n && ra <= cb) {
+          cyy[ra * 33 + cb] = v;
+          cyy[cb * 33 + ra] = v;
+        }
+      } else if (cb < 36 && ra < n) {
+        H.cxy[(cb - 32) * 32 + ra] = v;
+      }
+    }
+#else
     __syncwarp();
     if (warp == 0) {
       const double inv = 1.0 / (double)(m - 1);
@@ -482,6 +514,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         }
       (void)inv;
     }
+#endif
     __syncthreads();
     BM_PHASE(2);
     // ridge (estimators.py:148-150) and Cholesky (CovarianceBlocks._factor) on
@@ -966,12 +999,31 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
             P[bi * PS + 8 * ct + 2 * t4 + 1] = acc[2 * (r * 5 + ct) + 1];
           }
         }
+    }
+#if BM_BETA_PAR
+    // the 21 x n squared residuals (y0 - y~0(beta_g))[t]^2, one division each,
+    // on all threads (two barriers) instead of n divisions per lane on warp 0
+    __syncthreads();
+    for (int o = tid; o < NBETA * 32; o += NT) {
+      const int gi = o >> 5, t = o & 31;
+      if (t < n) {
+        const double d = y0[t] - P[gi * PS + t] / P[gi * PS + ONES_COL];
+        H.R1[gi * 33 + t] = __dmul_rn(d, d);
+      }
+    }
+    __syncthreads();
+#endif
+    if (warp == 0) {
       __syncwarp();
       // eps_g = ||y0 - y~0(beta_g)||^2 in NumPy's pairwise order; strict < argmin
       double eps = INFINITY;
       if (lane < NBETA) {
         const double S = P[lane * PS + ONES_COL];
-#if BM_CBETA
+#if BM_BETA_PAR
+        (void)S;
+        const double* sq = H.R1 + lane * 33;
+        eps = pairwise_sum_n(n, [&](int t) { return sq[t]; });
+#elif BM_CBETA
         // squares staged per lane (R1 is free after the reduction): one copy
         // of the division code instead of one per unrolled pairwise term
         double* sq = H.R1 + lane * 33;
