@@ -197,7 +197,7 @@ PHASES = ["gate", "means", "covariance", "cholesky", "linv", "quadforms", "dmin"
           "idl_pick", "idl_gather", "idl_estimate", "idl_writeback", "dep_wait", "patch_brl", "cta_life", "ctas",
           "sidl_setup", "sidl_screen", "sidl_ringsums", "sidl_scan", "sidl_dist_max", "sidl_exp_sum", "sidl_final", "sidl_count",
           "beta_loop_t0", "beta_loop_reduce", "loo_loops_t0", "nn_sorted", "nn_warp_merged", "nn_all_merged", "chol_linv", "chol_linv_stored",
-          "load_tile", "load_tile_cells", "load_tile_nbufs", "x43", "x44", "x45", "x46", "x47"]
+          "load_tile", "load_tile_cells", "load_tile_nbufs", "gate2_first", "gate2_rest", "gate2_sums", "gate2_scan", "gate2_count"]
 
 
 def phase_cycles(reset: bool = True) -> dict:

@@ -89,6 +89,9 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_COV_PAR
 #define BM_COV_PAR 1  // covariance epilogue: the divisions by m - 1 on all threads (bit-identical) (A/B)
 #endif
+#ifndef BM_CHOL_TRIM
+#define BM_CHOL_TRIM 1  // Cholesky: ridge on the lanes, incremental trailing-block indices, no dead L fill (bit-identical) (A/B)
+#endif
 #ifndef BM_TSTAGE
 #define BM_TSTAGE 1  // Gram staging / alpha: nearest rows on the lanes, transposed Wt / Vt / R / u (bit-identical) (A/B)
 #endif
@@ -521,11 +524,21 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     // warp 0; meanwhile warps 1..7 compute the Euclidean distances in NumPy's
     // order (optimize_alpha's nearest set, estimators.py:222)
     if (warp == 0) {
+#if BM_CHOL_TRIM
+      double ridge = 0.0;
+      if (lane == 0) {
+        const double tr = pairwise_sum_n(n, [&](int i) { return cyy[i * 33 + i]; });
+        ridge = tr > 0.0 ? 1e-6 * tr / n : 1e-6;
+      }
+      ridge = __shfl_sync(FULL, ridge, 0);
+      if (lane < n) cyy[lane * 33 + lane] += ridge;  // lane i: diagonal entry i
+#else
       if (lane == 0) {
         const double tr = pairwise_sum_n(n, [&](int i) { return cyy[i * 33 + i]; });
         const double ridge = tr > 0.0 ? 1e-6 * tr / n : 1e-6;
         for (int i = 0; i < n; i++) cyy[i * 33 + i] += ridge;
       }
+#endif
       __syncwarp();
       // Blocked right-looking Cholesky (8-column blocks) on warp 0: within a
       // block, lanes are rows and dot products run over the block's columns
@@ -552,6 +565,30 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         if (fail) break;
         // trailing update A[i][jj] -= sum_{k in block} L[i][k] L[jj][k], c1 <= jj <= i < n
         const int rem = n - c1;
+#if BM_CHOL_TRIM
+        if (rem > 0) {
+          // element e = lane + 32 s of the rem x rem trailing block: (row, col)
+          // advanced incrementally (one division per block, not two per element)
+          const int qd = 32 / rem, qm = 32 % rem;
+          int ri = lane / rem, ci = lane % rem;
+          for (int e = lane; e < rem * rem; e += 32) {
+            if (ci <= ri) {
+              const int i = c1 + ri, jj = c1 + ci;
+              double t = cyy[i * 33 + jj];
+#pragma unroll
+              for (int k = 0; k < 8; k++)
+                if (c0 + k < c1) t = fma(-L[i * 33 + c0 + k], L[jj * 33 + c0 + k], t);
+              cyy[i * 33 + jj] = t;
+            }
+            ri += qd;
+            ci += qm;
+            if (ci >= rem) {
+              ci -= rem;
+              ri++;
+            }
+          }
+        }
+#else
         for (int e = lane; e < rem * rem; e += 32) {
           const int i = c1 + e / rem, jj = c1 + e % rem;
           if (jj > i) continue;
@@ -561,8 +598,10 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
             if (c0 + k < c1) t = fma(-L[i * 33 + c0 + k], L[jj * 33 + c0 + k], t);
           cyy[i * 33 + jj] = t;
         }
+#endif
         __syncwarp();
       }
+#if !(BM_CHOL_TRIM && BM_LINV_ROLL)  // (the rolled L^-1 reads only L's lower triangle below row n)
       // the factor's lower triangle is complete; clear the upper part
       for (int j = 0; j < n; j++)
         if (lane < j) L[lane * 33 + j] = 0.0;
@@ -573,6 +612,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       }
       if (lane >= n)
         for (int j = 0; j < n; j++) L[lane * 33 + j] = 0.0;
+#endif
       __syncwarp();
       if (lane == 0) {
         H.fail = fail;

@@ -754,6 +754,20 @@ __device__ void gather(const KParams& P, CellSmem& S, int pr_t, int pc_t, bool g
     }
     __syncthreads();
     if (tid == 0) S.t_g[3] = clock64();
+#if BM_DIAG
+    // gate sub-phases of the patches that go past the first window (diagnostic)
+    if (tid == 0) {
+      if (e0 == 0 && !S.gated_stop) {
+        BM_DIAG_ADD(43, (S.t_g[3] - S.t_g[0]));  // first window: screening + accounting
+        S.t_pick = S.t_g[3];                     // (free until estimate_only's bookkeeping)
+      } else if (e0 != 0) {
+        BM_DIAG_ADD(44, (S.t_g[1] - S.t_pick));  // rest of the map screened
+        BM_DIAG_ADD(45, (S.t_g[2] - S.t_g[1]));  // its ring sums
+        BM_DIAG_ADD(46, (S.t_g[3] - S.t_g[2]));  // its nu scan
+        BM_DIAG_ADD(47, 1);
+      }
+    }
+#endif
     if (S.gated_stop) return;
   }
   if (tid == 0) {  // ungated: the whole map (_forced_estimate, profiles.py:148-149)
