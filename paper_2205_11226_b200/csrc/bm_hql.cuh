@@ -92,6 +92,12 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_CHOL_TRIM
 #define BM_CHOL_TRIM 1  // Cholesky: ridge on the lanes, incremental trailing-block indices, no dead L fill (bit-identical) (A/B)
 #endif
+#ifndef BM_QF_HOIST
+#define BM_QF_HOIST 1  // quadforms: L^-1 A fragments held in registers over the column tiles (N_y <= 24) (A/B)
+#endif
+#ifndef BM_LOO_HOIST
+#define BM_LOO_HOIST 1  // LOO: the pass's U A fragments / nearest index / d_i held in registers over the column tiles (A/B)
+#endif
 #ifndef BM_TSTAGE
 #define BM_TSTAGE 1  // Gram staging / alpha: nearest rows on the lanes, transposed Wt / Vt / R / u (bit-identical) (A/B)
 #endif
@@ -911,18 +917,34 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       for (int kk = 0; kk < 8; kk++) o[kk] = kk < 2 * NA ? y0r[kk] - zv.at(ry[kk], bB) : 0.0;
     };
     load_v(gw, fb);
+    // The L^-1 A fragments do not change over the column tiles; the d_j
+    // stores inside the loop keep the compiler from hoisting their loads, so
+    // (N_y <= 24: 12 fragments) they are held in registers explicitly.
+    constexpr bool HOIST = BM_QF_HOIST && NA <= 3;
+    constexpr int NLA = HOIST ? NA * (NA + 1) : 1;
+    double la[NLA];
+    if constexpr (HOIST) {
+      int q = 0;
+#pragma unroll
+      for (int r = 0; r < NA; r++)
+#pragma unroll
+        for (int kk = 0; kk < 2 * r + 2; kk++) la[q++] = H.Linv[(8 * r + g) * LS + 4 * kk + t4];
+    }
 #pragma unroll kQfUnroll
     for (int c = gw; c < nct; c += GWARPS) {
       load_v(c + GWARPS, fbn);
       double acc[8], acb[8];  // even / odd k-steps: two independent MMA chains
 #pragma unroll
       for (int i = 0; i < 8; i++) acc[i] = acb[i] = 0.0;
+      int q = 0;
 #pragma unroll
       for (int r = 0; r < NA; r++)
 #pragma unroll
         for (int kk = 0; kk < 2 * r + 2; kk++) {
-          if (kk & 1) dmma(acb[2 * r], acb[2 * r + 1], H.Linv[(8 * r + g) * LS + 4 * kk + t4], fb[kk]);
-          else dmma(acc[2 * r], acc[2 * r + 1], H.Linv[(8 * r + g) * LS + 4 * kk + t4], fb[kk]);
+          const double a = HOIST ? la[HOIST ? q : 0] : H.Linv[(8 * r + g) * LS + 4 * kk + t4];
+          q++;
+          if (kk & 1) dmma(acb[2 * r], acb[2 * r + 1], a, fb[kk]);
+          else dmma(acc[2 * r], acc[2 * r + 1], a, fb[kk]);
         }
 #pragma unroll
       for (int i = 0; i < 8; i++) acc[i] += acb[i];
@@ -1222,6 +1244,17 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
     for (int i = 0; i < 10 * RR; i++) acc[i] = 0.0;
     with_na(n, [&](auto NAc) {
     constexpr int NA = decltype(NAc)::value;
+#if BM_LOO_HOIST
+    // (RR == 1) the pass's row tile: its U A fragments, nearest index and d_i
+    // do not change over the column tiles; held in registers explicitly
+    static_assert(LOO_RR == 1, "hoisted A fragments assume one row tile per pass");
+    double ua[2 * NA];
+#pragma unroll
+    for (int kk = 0; kk < 2 * NA; kk++) ua[kk] = Un[(8 * r0 + g) * LS + 4 * kk + t4];
+    const int hi_ = 8 * r0 + g;
+    const int nri_h = hi_ < k ? H.near[hi_] : -2;
+    const double dni_h = hi_ < k ? H.dn[hi_] : 0.0;
+#endif
 #pragma unroll kLooUnroll
     for (int c = gw; c < nct; c += GWARPS) {
       // Gram B fragment of column tile c: (y0 - y_j)[4kk + t4] for j = 8c + g
@@ -1244,13 +1277,24 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         if (rr >= nrow) break;
         const int r = r0 + rr;
         const int i = 8 * r + g;
+#if BM_LOO_HOIST
+        const int nri = nri_h;
+        const double dni = dni_h;
+        (void)i;
+#else
         const int nri = i < k ? H.near[i] : -2;
         const double dni = i < k ? H.dn[i] : 0.0;
+#endif
         double g0 = 0.0, g1 = 0.0, h0 = 0.0, h1 = 0.0;  // two independent MMA chains
 #pragma unroll
         for (int kk = 0; kk < 2 * NA; kk += 2) {
+#if BM_LOO_HOIST
+          dmma(g0, g1, ua[kk], fv[kk]);
+          dmma(h0, h1, ua[kk + 1], fv[kk + 1]);
+#else
           dmma(g0, g1, Un[(8 * r + g) * LS + 4 * kk + t4], fv[kk]);
           dmma(h0, h1, Un[(8 * r + g) * LS + 4 * kk + 4 + t4], fv[kk + 1]);
+#endif
         }
         g0 += h0;
         g1 += h1;
