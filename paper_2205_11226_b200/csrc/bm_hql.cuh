@@ -98,6 +98,12 @@ constexpr int LS = 36;  // stride of Linv / Un: conflict-free A-fragment loads (
 #ifndef BM_LOO_HOIST
 #define BM_LOO_HOIST 1  // LOO: the pass's U A fragments / nearest index / d_i held in registers over the column tiles (A/B)
 #endif
+#ifndef BM_CHOL_UNR
+#define BM_CHOL_UNR 1  // Cholesky column: the block's dot product unrolled (loads together, same fma order) (A/B)
+#endif
+#ifndef BM_LINV_PAIR
+#define BM_LINV_PAIR 1  // L^-1 substitution two rows per step (shared loads, four chains; bit-identical) (A/B)
+#endif
 #ifndef BM_TSTAGE
 #define BM_TSTAGE 1  // Gram staging / alpha: nearest rows on the lanes, transposed Wt / Vt / R / u (bit-identical) (A/B)
 #endif
@@ -556,7 +562,14 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
           double t = 0.0;
           if (lane >= j && lane < n) {
             t = cyy[lane * 33 + j];
+#if BM_CHOL_UNR
+            // (the block's <= 7 earlier columns: loads issued together, the fma chain in the same order)
+#pragma unroll
+            for (int kk = 0; kk < 7; kk++)
+              if (c0 + kk < j) t = fma(-L[lane * 33 + c0 + kk], L[j * 33 + c0 + kk], t);
+#else
             for (int k = c0; k < j; k++) t = fma(-L[lane * 33 + k], L[j * 33 + k], t);
+#endif
           }
           const double sd = __shfl_sync(FULL, t, j);
           if (!(sd > 0.0)) { fail = true; break; }
@@ -633,6 +646,39 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
       // reads back only its own earlier stores), the even / odd partial sums
       // as in the unrolled form - the same bits in ~40 instructions instead
       // of ~1300 straight-line ones per patch (instruction fetch)
+#if BM_LINV_PAIR
+      // two rows per step (i even): rows i and i + 1 share the loads of the
+      // earlier rows' entries x_k, k < i, and run four independent fma chains;
+      // row i + 1 then adds its k = i term last, as the one-row loop does
+      int i = 0;
+#pragma unroll 1
+      for (; i + 1 < n; i += 2) {
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;
+#pragma unroll 2
+        for (int k = 0; k + 1 < i; k += 2) {
+          const double x0 = H.Linv[k * LS + lane], x1 = H.Linv[(k + 1) * LS + lane];
+          a0 = fma(L[i * 33 + k], x0, a0);
+          a1 = fma(L[i * 33 + k + 1], x1, a1);
+          b0 = fma(L[(i + 1) * 33 + k], x0, b0);
+          b1 = fma(L[(i + 1) * 33 + k + 1], x1, b1);
+        }
+        const double rd0 = H.rdiag[i], rd1 = H.rdiag[i + 1];
+        const double xi = lane > i ? 0.0 : (lane == i ? rd0 : -(a0 + a1) * rd0);
+        H.Linv[i * LS + lane] = xi;
+        b0 = fma(L[(i + 1) * 33 + i], xi, b0);
+        H.Linv[(i + 1) * LS + lane] = lane > i + 1 ? 0.0 : (lane == i + 1 ? rd1 : -(b0 + b1) * rd1);
+      }
+      if (i < n) {  // the last row of an odd n (i even: its k < i terms pair up)
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll 2
+        for (int k = 0; k + 1 < i; k += 2) {
+          s0 = fma(L[i * 33 + k], H.Linv[k * LS + lane], s0);
+          s1 = fma(L[i * 33 + k + 1], H.Linv[(k + 1) * LS + lane], s1);
+        }
+        const double rdi = H.rdiag[i];
+        H.Linv[i * LS + lane] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);
+      }
+#else
 #pragma unroll 1
       for (int i = 0; i < n; i++) {
         double s0 = 0.0, s1 = 0.0;
@@ -646,6 +692,7 @@ __device__ void hql_mma(const ZL& zv, int m, int n, const double* y0, HqlSmem& H
         const double rdi = H.rdiag[i];
         H.Linv[i * LS + lane] = lane > i ? 0.0 : (lane == i ? rdi : -(s0 + s1) * rdi);  // (lanes >= n: zeros)
       }
+#endif
       if (lane == 0) BM_DIAG_ADD(38, (clock64() - ph_t));  // + L^-1 (diagnostic)
       for (int i = n; i < 32; i++) H.Linv[i * LS + lane] = 0.0;  // zero beyond n
       if (lane == 0) BM_DIAG_ADD(39, (clock64() - ph_t));  // + Linv stored (diagnostic)
